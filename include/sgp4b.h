@@ -1,0 +1,104 @@
+/*
+ * sgp4b.h — C ABI of the B200-native SGP4 batch propagator.
+ *
+ * The reference package (`sgp4kit`, /root/reference/pkg) has no native
+ * boundary: its hot path is the Python API
+ *     init_batch()       pkg/src/sgp4kit/batch.py:92-109
+ *     propagate_batch()  pkg/src/sgp4kit/batch.py:166-205
+ *     sgp4_init()        pkg/src/sgp4kit/kernel.py:139-151
+ *     sgp4_propagate()   pkg/src/sgp4kit/kernel.py:513-534
+ *     solve_kepler()     pkg/src/sgp4kit/kernel.py:325-349
+ * Each entry point below replaces the numeric core of one of those calls;
+ * the Python mirror (paper_2603_27830_b200/) binds them with ctypes.
+ *
+ * Conventions
+ *   - Every pointer named *_dev is a device pointer on the current device;
+ *     the library never allocates, never synchronises and never aborts.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - Return 0 on success or a negative SGP4B_E* status.  The message of the
+ *     last failure on the calling thread is sgp4b_last_error().
+ *   - Per-cell anomalies (decay, eccentricity out of range …) are DATA in the
+ *     int32 code plane, never a status (kernel.py:45-52, 497-502).
+ *   - precision is 32 or 64 (batch.py:84-89); "T" below is float or double.
+ */
+#ifndef SGP4B_H
+#define SGP4B_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGP4B_OK 0
+#define SGP4B_EINVAL (-1)   /* bad argument (size, precision, null pointer) */
+#define SGP4B_ECUDA (-2)    /* CUDA launch/config error */
+
+/* Number of float slots in one satellite's SoA satrec (public SatInit float
+ * fields, kernel.py:64-107, in dataclass order). */
+#define SGP4B_SATREC_FIELDS 33
+/* Number of T slots in one packed propagate record. */
+#define SGP4B_RECORD_SLOTS 40
+
+/* grav: HOST pointer to 8 doubles {mu, radius_earth_km, xke, tumin, j2, j3,
+ * j4, j3oj2} (gravity.py:13-28); read at launch time. */
+
+/* Initialisation, one thread per satellite, always evaluated in fp64.
+ * Replaces _sgp4_init (kernel.py:154-322) incl. the epoch evaluation
+ * (kernel.py:316-322).
+ *   elements_dev : (7, n) fp64 SoA {no_kozai, ecco, inclo, nodeo, argpo, mo, bstar}
+ *   satrec_dev   : (33, n) fp64 SoA out, SatInit float fields in order
+ *   init_code_dev: (n) int32 out, error_code_at_init
+ *   isimp_dev    : (n) uint8 out
+ *   record_dev   : (n, 40) packed T records out (may be NULL) */
+int sgp4b_init(const double* elements_dev, int64_t n, const double* grav,
+               int precision, double* satrec_dev, int32_t* init_code_dev,
+               uint8_t* isimp_dev, void* record_dev, void* stream);
+
+/* Packs a (possibly user-edited) fp64 SoA satrec into propagate records.
+ * Used when a SatInit did not come from sgp4b_init (dataclasses.replace). */
+int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev,
+               const uint8_t* isimp_dev, int64_t n, const double* grav,
+               int precision, void* record_dev, void* stream);
+
+/* Dense grid: cell (i, j) = satellite i at times[j].  Replaces
+ * propagate_batch + _propagate + solve_kepler + the init-code merge
+ * (batch.py:166-205, kernel.py:325-534).
+ *   record_dev : (n, 40) packed T records
+ *   times_dev  : (m) T minutes since epoch
+ *   times_lo_dev: (m) float low words for precision 32 (t = hi + lo exactly
+ *                 as the caller's fp64 time), or NULL; ignored for 64
+ *   planes_dev : T base; plane p, row i, col j at
+ *                planes_dev[p*plane_stride + i*row_stride + j]
+ *   codes_dev  : int32 base; row i, col j at codes_dev[i*code_stride + j] */
+int sgp4b_propagate_grid(const void* record_dev, int64_t n,
+                         const void* times_dev, const float* times_lo_dev,
+                         int64_t m, int precision, const double* grav,
+                         void* planes_dev, int64_t plane_stride,
+                         int64_t row_stride, int32_t* codes_dev,
+                         int64_t code_stride, void* stream);
+
+/* Elementwise pairs: cell k = satellite sat_idx[k] at times[k].  Replaces
+ * the broadcasting scalar sgp4_propagate (kernel.py:513-534).
+ *   rv_dev : (6, p) T out; codes_dev : (p) int32 out. */
+int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev,
+                          const void* times_dev, const float* times_lo_dev,
+                          int64_t p, int precision, const double* grav,
+                          void* rv_dev, int32_t* codes_dev, void* stream);
+
+/* Newton solve of SGP4's Kepler equation, elementwise (kernel.py:325-349). */
+int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev,
+                       const void* u_dev, int64_t n, int precision,
+                       void* out_dev, void* stream);
+
+/* Thread-local message for the last non-zero status. */
+const char* sgp4b_last_error(void);
+
+/* ABI version (bumped on any signature or record-layout change). */
+int sgp4b_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGP4B_H */

@@ -1,0 +1,181 @@
+"""Device-side satrec state and the thin calls onto the C ABI.
+
+PyTorch is used only as the CUDA allocator / stream provider; every number
+is computed by libsgp4b.so.  Nothing here falls back to the CPU: without a
+CUDA device the calls raise.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .gravity import GravityModel
+
+SATREC_FIELDS = _native.SATREC_FIELDS
+RECORD_SLOTS = _native.RECORD_SLOTS
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2603_27830_b200 needs a CUDA device (B200, sm_100a); "
+            "there is no CPU fallback")
+    _native.load()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {device}")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+def torch_dtype(precision: int) -> torch.dtype:
+    return torch.float32 if precision == 32 else torch.float64
+
+
+def np_dtype(precision: int):
+    return np.float32 if precision == 32 else np.float64
+
+
+def precision_of(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return 32
+    if dt == np.float64:
+        return 64
+    raise ValueError(f"dtype must be float32 or float64, got {dt}")
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+@dataclass
+class DeviceSatrec:
+    """All per-satellite state of one batch, resident on one GPU.
+
+    satrec : (33, n) fp64, SatInit float fields in dataclass order
+    codes  : (n,) int32 error_code_at_init
+    isimp  : (n,) uint8
+    record : (n, 40) packed propagate records at the batch precision
+    """
+
+    satrec: torch.Tensor
+    codes: torch.Tensor
+    isimp: torch.Tensor
+    record: torch.Tensor
+    precision: int
+    grav: GravityModel
+    device: torch.device
+
+    @property
+    def n(self) -> int:
+        return int(self.codes.shape[0])
+
+
+_GRAV_CACHE: dict = {}
+
+
+def _grav_host(grav: GravityModel, device) -> np.ndarray:
+    # the C ABI reads grav[8] on the host (kernel launch parameter)
+    key = (grav, str(device))
+    arr = _GRAV_CACHE.get(key)
+    if arr is None:
+        arr = grav.as_array()
+        _GRAV_CACHE[key] = arr
+    return arr
+
+
+def _host_ptr(arr: np.ndarray) -> int:
+    return arr.ctypes.data
+
+
+def init_device(elements: np.ndarray, grav: GravityModel, precision: int,
+                device=None) -> DeviceSatrec:
+    """(7, n) fp64 element columns -> DeviceSatrec via the init kernel."""
+    device = require_cuda(device)
+    elements = np.ascontiguousarray(elements, dtype=np.float64)
+    n = elements.shape[1]
+    el = torch.from_numpy(elements).to(device, non_blocking=False)
+    return init_device_tensor(el, grav, precision, device)
+
+
+def init_device_tensor(el: torch.Tensor, grav: GravityModel, precision: int,
+                       device=None) -> DeviceSatrec:
+    """Same as :func:`init_device` for (7, n) fp64 columns already on the GPU."""
+    device = require_cuda(device if device is not None else el.device)
+    n = int(el.shape[1])
+    satrec = torch.empty((SATREC_FIELDS, n), dtype=torch.float64, device=device)
+    codes = torch.empty((n,), dtype=torch.int32, device=device)
+    isimp = torch.empty((n,), dtype=torch.uint8, device=device)
+    record = torch.empty((n, RECORD_SLOTS), dtype=torch_dtype(precision), device=device)
+    g = _grav_host(grav, device)
+    with torch.cuda.device(device):
+        _native.check(_native.load().sgp4b_init(
+            el.data_ptr(), n, _host_ptr(g), precision, satrec.data_ptr(),
+            codes.data_ptr(), isimp.data_ptr(), record.data_ptr(), _stream(device)))
+    return DeviceSatrec(satrec, codes, isimp, record, precision, grav, device)
+
+
+def pack_device(satrec64: np.ndarray, codes: np.ndarray, isimp: np.ndarray,
+                grav: GravityModel, precision: int, device=None) -> DeviceSatrec:
+    """Host SoA fields (e.g. from a user-built SatInit) -> packed records."""
+    device = require_cuda(device)
+    n = satrec64.shape[1]
+    sr = torch.from_numpy(np.ascontiguousarray(satrec64, dtype=np.float64)).to(device)
+    cd = torch.from_numpy(np.ascontiguousarray(codes, dtype=np.int32)).to(device)
+    si = torch.from_numpy(np.ascontiguousarray(isimp, dtype=np.uint8)).to(device)
+    record = torch.empty((n, RECORD_SLOTS), dtype=torch_dtype(precision), device=device)
+    g = _grav_host(grav, device)
+    with torch.cuda.device(device):
+        _native.check(_native.load().sgp4b_pack(
+            sr.data_ptr(), cd.data_ptr(), si.data_ptr(), n, _host_ptr(g), precision,
+            record.data_ptr(), _stream(device)))
+    return DeviceSatrec(sr, cd, si, record, precision, grav, device)
+
+
+def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,
+                   codes: torch.Tensor, times_lo: torch.Tensor | None = None,
+                   rows: tuple[int, int] | None = None) -> None:
+    """Launch the grid kernel: planes (6, n, m) and codes (n, m) device
+    tensors (any strides with unit column stride) receive the grid.
+
+    ``rows=(r0, r1)`` propagates only satellites r0..r1 into row 0.. of the
+    outputs (used by tiling and by the streamed API).
+    """
+    r0, r1 = rows if rows is not None else (0, dev.n)
+    n = r1 - r0
+    m = int(times.shape[0])
+    if planes.stride(2) != 1 or codes.stride(1) != 1:
+        raise ValueError("output columns must be contiguous")
+    rec = dev.record[r0:r1]
+    g = _grav_host(dev.grav, dev.device)
+    _native.check(_native.load().sgp4b_propagate_grid(
+        rec.data_ptr(), n, times.data_ptr(), _native.ptr(times_lo), m, dev.precision,
+        _host_ptr(g), planes.data_ptr(), planes.stride(0), planes.stride(1),
+        codes.data_ptr(), codes.stride(0), _stream(dev.device)))
+
+
+def propagate_pairs(dev: DeviceSatrec, sat_idx: torch.Tensor, times: torch.Tensor,
+                    rv: torch.Tensor, codes: torch.Tensor) -> None:
+    p = int(times.shape[0])
+    g = _grav_host(dev.grav, dev.device)
+    _native.check(_native.load().sgp4b_propagate_pairs(
+        dev.record.data_ptr(), sat_idx.data_ptr(), times.data_ptr(), None, p,
+        dev.precision, _host_ptr(g), rv.data_ptr(), codes.data_ptr(),
+        _stream(dev.device)))
+
+
+def solve_kepler_device(axnl: torch.Tensor, aynl: torch.Tensor, u: torch.Tensor,
+                        precision: int) -> torch.Tensor:
+    out = torch.empty_like(u)
+    _native.check(_native.load().sgp4b_solve_kepler(
+        axnl.data_ptr(), aynl.data_ptr(), u.data_ptr(), int(u.numel()), precision,
+        out.data_ptr(), _stream(u.device)))
+    return out

@@ -1,0 +1,336 @@
+"""Batch API (mirror of sgp4kit.batch, batch.py:54-269), GPU-backed.
+
+``init_batch`` runs one init kernel over the whole catalogue and leaves the
+packed satrec resident on the GPU; ``propagate_batch`` runs one grid kernel
+that writes the reference's (6, N, M) planes + (N, M) int32 codes layout
+directly, then copies it to pinned host memory.  ``propagate_batch_device``
+is the same call with the grid left in HBM (torch tensors), the form the
+multi-GPU sharding and the throughput benchmark use.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from typing import Any, Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _device
+from .gravity import WGS72, GravityModel
+from .kernel import SatInit, satinit_from_device, _device_of
+from .tle import MeanElements, elements_to_columns
+
+PLANE_NAMES = ("rx", "ry", "rz", "vx", "vy", "vz")
+
+MAGIC = b"SGB1"
+_HEADER = struct.Struct("<4sQQI8s")        # magic, N, M, precision bits, tag
+PLANE_ORDER_TAG = b"rrrvvve\x00"
+
+DEFAULT_TILE_CELLS = 1 << 18
+
+
+class GridAllocationError(MemoryError):
+    """The output grid could not be allocated (batch.py:33-41)."""
+
+    def __init__(self, n: int, m: int, nbytes: int):
+        super().__init__(f"cannot allocate {n}x{m} output grid ({nbytes} bytes)")
+        self.n = n
+        self.m = m
+        self.nbytes = nbytes
+
+
+class StreamAborted(RuntimeError):
+    """A streaming sink raised; carries the tiles already delivered."""
+
+    def __init__(self, tiles_completed: int, cause: BaseException):
+        super().__init__(f"sink failed after {tiles_completed} tiles: {cause}")
+        self.tiles_completed = tiles_completed
+        self.__cause__ = cause
+
+
+class SatBatch:
+    """Structure-of-arrays satellite batch of length ``n`` (batch.py:54-63).
+
+    Holds the GPU-resident satrec; ``.init`` materialises the host
+    :class:`SatInit` on first access.
+    """
+
+    def __init__(self, init: SatInit | None = None, n: int | None = None, *,
+                 device_satrec: "_device.DeviceSatrec | None" = None):
+        if device_satrec is None:
+            if init is None:
+                raise ValueError("SatBatch needs init or device_satrec")
+            device_satrec, shape = _device_of(init)
+            if len(shape) != 1:
+                raise ValueError("SatBatch init fields must be 1-D")
+        self._dev = device_satrec
+        self._init = init
+        self.n = int(n if n is not None else device_satrec.n)
+        if self.n != device_satrec.n:
+            raise ValueError(f"n={self.n} does not match the satrec length {device_satrec.n}")
+
+    @property
+    def device_satrec(self) -> "_device.DeviceSatrec":
+        return self._dev
+
+    @property
+    def precision(self) -> int:
+        return self._dev.precision
+
+    @property
+    def dtype(self):
+        return _device.np_dtype(self._dev.precision)
+
+    @property
+    def init(self) -> SatInit:
+        if self._init is None:
+            self._init = satinit_from_device(self._dev, (self.n,))
+        return self._init
+
+    @property
+    def error_codes(self) -> np.ndarray:
+        return self._dev.codes.cpu().numpy().astype(np.int32)
+
+    def __repr__(self) -> str:
+        return f"SatBatch(n={self.n}, precision={self.precision}, device={self._dev.device})"
+
+
+@dataclass(frozen=True)
+class BatchResult:
+    """Dense grid: planes (6, N, M) and error codes (N, M) (batch.py:66-81)."""
+
+    planes: Any
+    error: Any
+    n: int
+    m: int
+
+    @property
+    def r(self):
+        return _moveaxis(self.planes[:3])
+
+    @property
+    def v(self):
+        return _moveaxis(self.planes[3:])
+
+
+def _moveaxis(x):
+    if isinstance(x, torch.Tensor):
+        return torch.movedim(x, 0, -1)
+    return np.moveaxis(x, 0, -1)
+
+
+def _precision(precision: int) -> int:
+    if precision not in (32, 64):
+        raise ValueError(f"precision must be 32 or 64, got {precision}")
+    return precision
+
+
+def init_batch(elements: Sequence[MeanElements], grav: GravityModel = WGS72,
+               precision: int = 64, device=None) -> SatBatch:
+    """Initialise many satellites at once (batch.py:92-109) on the GPU.
+
+    ``elements`` may also be a (7, n) fp64 array in ELEMENT_COLUMNS order
+    (e.g. from :func:`~paper_2603_27830_b200.tle.parse_catalog_columns`).
+    Never raises on bad elements: codes land in ``.error_codes``.
+    """
+    if isinstance(elements, np.ndarray):
+        cols = np.asarray(elements, dtype=np.float64)
+        if cols.ndim != 2 or cols.shape[0] != 7:
+            raise ValueError("element columns must have shape (7, n)")
+        if cols.shape[1] == 0:
+            raise ValueError("empty element list")
+    else:
+        if not elements:
+            raise ValueError("empty element list")
+        cols = elements_to_columns(elements)
+    precision = _precision(precision)
+    dev = _device.init_device(cols, grav, precision, device)
+    return SatBatch(device_satrec=dev)
+
+
+def _times(sats: SatBatch, times) -> np.ndarray:
+    t = np.asarray(times, dtype=sats.dtype)
+    if t.ndim != 1 or t.size == 0:
+        raise ValueError("times must be a non-empty 1-D array")
+    return t
+
+
+def _alloc_grid(n: int, m: int, precision: int, device, pin: bool = False):
+    tdt = _device.torch_dtype(precision)
+    itemsize = 4 if precision == 32 else 8
+    try:
+        if device == "cpu":
+            planes = torch.empty((6, n, m), dtype=tdt, pin_memory=pin)
+            error = torch.empty((n, m), dtype=torch.int32, pin_memory=pin)
+        else:
+            planes = torch.empty((6, n, m), dtype=tdt, device=device)
+            error = torch.empty((n, m), dtype=torch.int32, device=device)
+    except (torch.cuda.OutOfMemoryError, RuntimeError, MemoryError) as exc:
+        if isinstance(exc, RuntimeError) and "memory" not in str(exc).lower():
+            raise
+        raise GridAllocationError(n, m, 6 * n * m * itemsize + 4 * n * m) from None
+    return planes, error
+
+
+def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
+                           times_lo=None) -> BatchResult:
+    """Propagate every satellite to every time, leaving the grid in HBM.
+
+    ``times`` is a 1-D array/tensor (cast to the batch dtype); ``out`` may
+    supply preallocated (planes, error) device tensors.  ``times_lo``
+    (fp32 batches only) carries the low words of fp64 times for the
+    double-float secular stage.  Returns a BatchResult of torch tensors.
+    """
+    dev = sats.device_satrec
+    with torch.cuda.device(dev.device):
+        if isinstance(times, torch.Tensor):
+            t_d = times.to(device=dev.device, dtype=_device.torch_dtype(dev.precision))
+            if t_d.ndim != 1 or t_d.numel() == 0:
+                raise ValueError("times must be a non-empty 1-D array")
+        else:
+            t_d = torch.from_numpy(_times(sats, times)).to(dev.device)
+        t_d = t_d.contiguous()
+        m = int(t_d.shape[0])
+        if out is None:
+            planes, error = _alloc_grid(sats.n, m, dev.precision, dev.device)
+        else:
+            planes, error = out
+        _device.propagate_grid(dev, t_d, planes, error, times_lo=times_lo)
+    return BatchResult(planes=planes, error=error, n=sats.n, m=m)
+
+
+def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchResult:
+    """Propagate every satellite to every time (batch.py:166-205).
+
+    Cell (i, j) is bitwise equal to ``sgp4_propagate`` of satellite i at
+    time j at the batch precision.  ``workers`` is accepted for API
+    compatibility; it never affected output and the GPU needs no pool.
+    Returns numpy arrays backed by pinned host memory.
+    """
+    t = _times(sats, times)
+    dev = sats.device_satrec
+    n, m = sats.n, t.size
+    with torch.cuda.device(dev.device):
+        stream = torch.cuda.current_stream(dev.device)
+        t_h = torch.from_numpy(t).pin_memory()
+        t_d = t_h.to(dev.device, non_blocking=True)
+        res = propagate_batch_device(sats, t_d)
+        planes_h, error_h = _alloc_grid(n, m, dev.precision, "cpu", pin=True)
+        planes_h.copy_(res.planes, non_blocking=True)
+        error_h.copy_(res.error, non_blocking=True)
+        stream.synchronize()
+    return BatchResult(planes=planes_h.numpy(), error=error_h.numpy(), n=n, m=m)
+
+
+def partition_work(n: int, m: int, workers: int) -> list[tuple[int, int]]:
+    """Balanced disjoint covering ranges over the flat N*M index space
+    (batch.py:125-141); also the rule used to shard satellites over GPUs."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    total = n * m
+    k = min(workers, total)
+    if k <= 0:
+        return []
+    base, extra = divmod(total, k)
+    bounds = np.concatenate([[0], np.cumsum([base + (i < extra) for i in range(k)])])
+    return [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:])]
+
+
+def _tile_grid(n: int, m: int, tile_rows: int, tile_cols: int):
+    """Row-major (row-slice, col-slice) tiles covering N x M."""
+    return [(slice(r, min(r + tile_rows, n)), slice(c, min(c + tile_cols, m)))
+            for r in range(0, n, tile_rows) for c in range(0, m, tile_cols)]
+
+
+@dataclass(frozen=True)
+class StreamSummary:
+    cells_emitted: int
+    nonzero_error_count: int
+
+
+def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: int,
+                             sink: Callable[[slice, slice, np.ndarray, np.ndarray], Any]
+                             ) -> StreamSummary:
+    """Tile-by-tile propagation without a full host grid (batch.py:214-241).
+
+    Tiles are delivered in row-major order.  The GPU computes and copies
+    tile k+1 into pinned memory while the sink consumes tile k; peak host
+    memory is two tiles.  A sink exception aborts with the count delivered.
+    """
+    if tile_rows < 1 or tile_cols < 1:
+        raise ValueError("tile dimensions must be >= 1")
+    t = np.asarray(times, dtype=sats.dtype)
+    if t.ndim != 1:
+        raise ValueError("times must be a 1-D array")
+    dev = sats.device_satrec
+    n, m = sats.n, t.size
+    tiles = _tile_grid(n, m, tile_rows, tile_cols)
+    if not tiles:
+        return StreamSummary(0, 0)
+    cells = errors = completed = 0
+    with torch.cuda.device(dev.device):
+        stream = torch.cuda.current_stream(dev.device)
+        t_d = torch.from_numpy(t).to(dev.device)
+
+        def launch(tile):
+            rows, cols = tile
+            tr, tc = rows.stop - rows.start, cols.stop - cols.start
+            planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
+            _device.propagate_grid(dev, t_d[cols], planes_d, err_d,
+                                   rows=(rows.start, rows.stop))
+            planes_h, err_h = _alloc_grid(tr, tc, dev.precision, "cpu", pin=True)
+            planes_h.copy_(planes_d, non_blocking=True)
+            err_h.copy_(err_d, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+            return planes_h, err_h, done, (planes_d, err_d)
+
+        pending = launch(tiles[0])
+        for k, (rows, cols) in enumerate(tiles):
+            planes_h, err_h, done, _keep = pending
+            pending = launch(tiles[k + 1]) if k + 1 < len(tiles) else None
+            done.synchronize()
+            planes_np, err_np = planes_h.numpy(), err_h.numpy()
+            try:
+                sink(rows, cols, planes_np, err_np)
+            except Exception as exc:
+                if pending is not None:
+                    pending[2].synchronize()
+                raise StreamAborted(completed, exc) from exc
+            completed += 1
+            cells += err_np.size
+            errors += int(np.count_nonzero(err_np))
+    return StreamSummary(cells_emitted=cells, nonzero_error_count=errors)
+
+
+def write_grid_binary(result: BatchResult, stream) -> None:
+    """SGB1: 32-byte little-endian header, planes rx..vz, then int32 codes
+    (batch.py:244-251).  Device results are copied out plane by plane."""
+    planes = result.planes
+    if isinstance(planes, torch.Tensor):
+        planes = planes.cpu().numpy()
+    error = result.error.cpu().numpy() if isinstance(result.error, torch.Tensor) else result.error
+    itemsize = np.dtype(planes.dtype).itemsize
+    stream.write(_HEADER.pack(MAGIC, result.n, result.m, itemsize * 8, PLANE_ORDER_TAG))
+    le = np.dtype(f"<f{itemsize}")
+    for plane in planes:
+        stream.write(np.ascontiguousarray(plane, dtype=le).tobytes())
+    stream.write(np.ascontiguousarray(error, dtype="<i4").tobytes())
+
+
+def read_grid_binary(stream) -> BatchResult:
+    """Inverse of :func:`write_grid_binary`."""
+    magic, n, m, bits, tag = _HEADER.unpack(stream.read(_HEADER.size))
+    if magic != MAGIC:
+        raise ValueError(f"bad magic: {magic!r}")
+    if tag != PLANE_ORDER_TAG:
+        raise ValueError(f"unknown plane order tag: {tag!r}")
+    if bits not in (32, 64):
+        raise ValueError(f"precision must be 32 or 64, got {bits}")
+    itemsize = bits // 8
+    planes = np.frombuffer(stream.read(6 * n * m * itemsize), dtype=f"<f{itemsize}")
+    planes = planes.reshape(6, n, m).astype(np.float32 if bits == 32 else np.float64)
+    error = np.frombuffer(stream.read(4 * n * m), dtype="<i4").reshape(n, m)
+    return BatchResult(planes=planes, error=error.astype(np.int32), n=n, m=m)

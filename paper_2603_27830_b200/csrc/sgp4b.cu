@@ -1,0 +1,1074 @@
+// sgp4b.cu — B200 (sm_100a) SGP4 near-Earth batch propagator.
+//
+// Kernels
+//   init_kernel        1 thread / satellite, fp64.  _sgp4_init, kernel.py:154-322
+//   pack_kernel        1 thread / satellite.  SoA satrec -> packed record
+//   grid_kernel<T>     1 warp = 1 satellite x 128 time steps (4 per lane);
+//                      _propagate + solve_kepler + merge, kernel.py:325-534,
+//                      over the dense grid of propagate_batch, batch.py:166-205
+//   pairs_kernel<T>    1 thread / (satellite, time) pair; sgp4_propagate's
+//                      broadcasting form, kernel.py:513-534
+//   kepler_kernel<T>   solve_kepler, kernel.py:325-349
+//
+// Numerics
+//   * fp64 cells follow the reference operation order and its guarded
+//     both-branch selects (dmath.py:199-221); transcendental calls are
+//     CUDA's correctly-rounded-to-1ulp libdevice routines.
+//   * fp32 cells are the throughput path: per-satellite work is hoisted into
+//     the packed record at init time (computed in fp64, rounded once), the
+//     secular angles are formed in double-float (hi/lo pairs) and reduced
+//     mod 2*pi before anything is rounded to fp32, sin/cos/rcp/rsqrt use the
+//     SFU (MUFU) pipe, Kepler runs a warp-uniform fixed iteration count
+//     chosen from the satellite's eccentricity, atan2 + three of the
+//     sincos evaluations of the short-period stage are replaced by exact
+//     rotations by small angles.
+//   * Error codes follow _first_error precedence 2 > 1 > 4 > 6 and the
+//     init-code merge of kernel.py:497-502, 529-534.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include <float.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/sgp4b.h"
+
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr double kInvTwoPi = 0.15915494309189533576888376337251;
+constexpr double kX2o3 = 2.0 / 3.0;
+
+// 2*pi split for float Cody-Waite reduction: hi has 8 trailing zero bits so
+// k*hi is exact for |k| < 2^8 ... we rely on fmaf exactness instead (see
+// reduce2pi_f): hi is the float nearest 2*pi, lo the float nearest the rest.
+constexpr float kTwoPiHiF = 6.28318548202514648437f;     // float(2*pi)
+constexpr float kTwoPiLoF = -1.7484556000744487e-07f;    // 2*pi - hi
+constexpr float kInvTwoPiF = 0.159154943091895335768883763372514f;
+
+struct Grav {
+  double mu, re, xke, tumin, j2, j3, j4, j3oj2;
+};
+
+// ---- SoA satrec fields: SatInit float fields in dataclass order --------
+// kernel.py:68-107
+enum Field {
+  F_NO_KOZAI = 0, F_ECCO, F_INCLO, F_NODEO, F_ARGPO, F_MO, F_BSTAR,
+  F_NO_UNKOZAI, F_AO, F_CON41, F_X1MTH2, F_X7THM1,
+  F_MDOT, F_ARGPDOT, F_NODEDOT, F_NODECF,
+  F_CC1, F_CC4, F_CC5, F_D2, F_D3, F_D4, F_T2COF, F_T3COF, F_T4COF, F_T5COF,
+  F_ETA, F_OMGCOF, F_XMCOF, F_DELMO, F_SINMAO, F_AYCOF, F_XLCOF,
+  F_COUNT
+};
+static_assert(F_COUNT == SGP4B_SATREC_FIELDS, "satrec field count");
+
+// ---- packed propagate record (one per satellite, 40 T slots) ----------
+enum Slot {
+  S_MO = 0, S_MDOT, S_ARGPO, S_ARGPDOT, S_NODEO, S_NODEDOT, S_NODECF, S_CC1,
+  S_BC4, S_T2COF, S_OMGCOF, S_ETA, S_XMCOF, S_DELMO, S_D2, S_D3,
+  S_D4, S_BC5, S_SINMAO, S_T3COF, S_T4COF, S_T5COF, S_NO, S_AM0,
+  S_ECCO, S_INCLO, S_SINIO, S_COSIO, S_AYCOF, S_XLCOF, S_CON41, S_X1MTH2,
+  S_X7THM1, S_FLAGS,
+  // fp32 double-float secular support (low words; zero in fp64 records)
+  S_MDOT_LO, S_ARGPDOT_LO, S_NODEDOT_LO, S_UDOT, S_UDOT_LO, S_U0,
+  S_COUNT
+};
+static_assert(S_COUNT == SGP4B_RECORD_SLOTS, "record slot count");
+
+// flags word
+constexpr int FLAG_ISIMP = 1;
+constexpr int FLAG_BAD_NM = 2;
+constexpr int KEPLER_SHIFT = 4;   // 4 bits: fixed Kepler iterations (fp32)
+constexpr int CODE_SHIFT = 8;     // 8 bits: persistent init code
+
+// ---- error plumbing ----------------------------------------------------
+thread_local char g_last_error[512] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(SGP4B_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return SGP4B_OK;
+}
+
+// ======================================================================
+// fp64 helpers with the reference's select semantics
+// ======================================================================
+
+// dmath.maximum(x, floor) == where(x >= floor, x, floor)   dmath.py:213-215
+__device__ __forceinline__ double gmax(double x, double f) { return x >= f ? x : f; }
+__device__ __forceinline__ float gmaxf(float x, float f) { return x >= f ? x : f; }
+
+// C fmod(x, 2*pi), exact: with the right integer quotient q the remainder
+// x - q*2pi is representable, so one fma produces it without rounding.
+__device__ __forceinline__ double fmod_2pi(double x) {
+  if (!(fabs(x) < 1.0e15)) return fmod(x, kTwoPi);
+  double q = trunc(x * kInvTwoPi);
+  double r = fma(-q, kTwoPi, x);
+  if (x >= 0.0) {
+    if (r < 0.0) { q -= 1.0; r = fma(-q, kTwoPi, x); }
+    else if (r >= kTwoPi) { q += 1.0; r = fma(-q, kTwoPi, x); }
+  } else {
+    if (r > 0.0) { q += 1.0; r = fma(-q, kTwoPi, x); }
+    else if (r <= -kTwoPi) { q -= 1.0; r = fma(-q, kTwoPi, x); }
+  }
+  return r;
+}
+
+// numpy remainder (Python floor-mod) by 2*pi: npy_divmod semantics.
+__device__ __forceinline__ double pymod_2pi(double x) {
+  double r = fmod_2pi(x);
+  if (r != 0.0) {
+    if (r < 0.0) r += kTwoPi;
+  } else {
+    r = 0.0;
+  }
+  return r;
+}
+
+// ======================================================================
+// Record (register-resident copy of one satellite's packed record)
+// ======================================================================
+template <typename T>
+struct Rec {
+  T v[S_COUNT];
+  __device__ __forceinline__ int flags() const;
+};
+template <>
+__device__ __forceinline__ int Rec<float>::flags() const { return __float_as_int(v[S_FLAGS]); }
+template <>
+__device__ __forceinline__ int Rec<double>::flags() const {
+  return (int)__double_as_longlong(v[S_FLAGS]);
+}
+
+__device__ __forceinline__ void load_rec(const float* __restrict__ p, Rec<float>& r) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < S_COUNT / 4; ++i) {
+    float4 x = __ldg(q + i);
+    r.v[4 * i + 0] = x.x; r.v[4 * i + 1] = x.y; r.v[4 * i + 2] = x.z; r.v[4 * i + 3] = x.w;
+  }
+}
+__device__ __forceinline__ void load_rec(const double* __restrict__ p, Rec<double>& r) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < S_COUNT / 2; ++i) {
+    double2 x = __ldg(q + i);
+    r.v[2 * i + 0] = x.x; r.v[2 * i + 1] = x.y;
+  }
+}
+
+
+// ======================================================================
+// Kepler (kernel.py:325-349)
+// ======================================================================
+template <typename T>
+__device__ __forceinline__ T kepler_reference(T axnl, T aynl, T u) {
+  const T clamp = T(0.95);
+  T eo1 = u;
+  bool active = true;
+#pragma unroll 1
+  for (int it = 0; it < 10 && active; ++it) {
+    T s, c;
+    sincos(eo1, &s, &c);
+    T den = T(1) - c * axnl - s * aynl;
+    T tem5 = (u - aynl * c + axnl * s - eo1) / den;
+    tem5 = tem5 >= clamp ? clamp : (tem5 <= -clamp ? -clamp : tem5);
+    eo1 = eo1 + tem5;
+    active = fabs(tem5) >= T(1.0e-12);
+  }
+  return eo1;
+}
+template <>
+__device__ __forceinline__ float kepler_reference<float>(float axnl, float aynl, float u) {
+  const float clamp = 0.95f;
+  float eo1 = u;
+  bool active = true;
+#pragma unroll 1
+  for (int it = 0; it < 10 && active; ++it) {
+    float s, c;
+    sincosf(eo1, &s, &c);
+    float den = 1.0f - c * axnl - s * aynl;
+    float tem5 = (u - aynl * c + axnl * s - eo1) / den;
+    tem5 = tem5 >= clamp ? clamp : (tem5 <= -clamp ? -clamp : tem5);
+    eo1 = eo1 + tem5;
+    active = fabsf(tem5) >= 1.0e-12f;
+  }
+  return eo1;
+}
+
+// ======================================================================
+// fp64 cell: the reference operation order (kernel.py:352-510)
+// ======================================================================
+struct Cell64 {
+  double r[3], v[3];
+  int code;
+};
+
+__device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Grav& g, Cell64& o) {
+  const double tiny = DBL_MIN;
+  const double xke = g.xke, j2 = g.j2, re = g.re;
+  const double vkmpersec = re * xke / 60.0;
+  const int flags = R.flags();
+  const bool isimp = flags & FLAG_ISIMP;
+
+  // secular gravity and atmospheric drag  kernel.py:365-391
+  double xmdf = R.v[S_MO] + R.v[S_MDOT] * t;
+  double argpdf = R.v[S_ARGPO] + R.v[S_ARGPDOT] * t;
+  double nodedf = R.v[S_NODEO] + R.v[S_NODEDOT] * t;
+  double t2 = t * t;
+  double nodem = nodedf + R.v[S_NODECF] * t2;
+  double tempa = 1.0 - R.v[S_CC1] * t;
+  double tempe = R.v[S_BC4] * t;
+  double templ = R.v[S_T2COF] * t2;
+  double mm = xmdf, argpm = argpdf;
+  if (!isimp) {
+    double delomg = R.v[S_OMGCOF] * t;
+    double delmtemp = 1.0 + R.v[S_ETA] * cos(xmdf);
+    double delm = R.v[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R.v[S_DELMO]);
+    double temp = delomg + delm;
+    mm = xmdf + temp;
+    argpm = argpdf - temp;
+    double t3 = t2 * t;
+    double t4 = t3 * t;
+    tempa = tempa - R.v[S_D2] * t2 - R.v[S_D3] * t3 - R.v[S_D4] * t4;
+    tempe = tempe + R.v[S_BC5] * (sin(mm) - R.v[S_SINMAO]);
+    templ = templ + R.v[S_T3COF] * t3 + t4 * (R.v[S_T4COF] + t * R.v[S_T5COF]);
+  }
+
+  // mean motion / eccentricity update  kernel.py:393-414
+  const bool bad_nm = flags & FLAG_BAD_NM;
+  double am = R.v[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
+  double am_safe = gmax(am, tiny);
+  double nm = xke / pow(am_safe, 1.5);
+  double em = R.v[S_ECCO] - tempe;
+  const bool bad_em = (em >= 1.0) || (em < -0.001);
+  em = em < 1.0e-6 ? 1.0e-6 : em;
+  mm = mm + R.v[S_NO] * templ;
+  double xlm = mm + argpm + nodem;
+  nodem = fmod_2pi(nodem);              // mod_twopi_signed, dmath.py:218-221
+  argpm = pymod_2pi(argpm);
+  xlm = pymod_2pi(xlm);
+  mm = pymod_2pi(xlm - argpm - nodem);
+
+  const double sinip = R.v[S_SINIO];
+  const double cosip = R.v[S_COSIO];
+
+  // long-period periodics  kernel.py:419-431
+  double ep = em;
+  double sa, ca;
+  sincos(argpm, &sa, &ca);
+  double axnl = ep * ca;
+  double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
+  double temp = 1.0 / pl_lp;
+  double aynl = ep * sa + temp * R.v[S_AYCOF];
+  double xl = mm + argpm + nodem + temp * R.v[S_XLCOF] * axnl;
+
+  // Kepler  kernel.py:434-437
+  double u = pymod_2pi(xl - nodem);
+  double eo1 = kepler_reference<double>(axnl, aynl, u);
+  double sineo1, coseo1;
+  sincos(eo1, &sineo1, &coseo1);
+
+  // short-period preliminaries  kernel.py:440-460
+  double ecose = axnl * coseo1 + aynl * sineo1;
+  double esine = axnl * sineo1 - aynl * coseo1;
+  double el2 = axnl * axnl + aynl * aynl;
+  double pl = am_safe * (1.0 - el2);
+  const bool bad_pl = pl < 0.0;
+  double pl_safe = gmax(pl, tiny);
+  double rl = am_safe * (1.0 - ecose);
+  double rl_safe = rl == 0.0 ? tiny : rl;
+  double rdotl = sqrt(am_safe) * esine / rl_safe;
+  double rvdotl = sqrt(pl_safe) / rl_safe;
+  double betal = sqrt(gmax(1.0 - el2, tiny));
+  temp = esine / (1.0 + betal);
+  double sinu = am_safe / rl_safe * (sineo1 - aynl - axnl * temp);
+  double cosu = am_safe / rl_safe * (coseo1 - axnl + aynl * temp);
+  double su = atan2(sinu, cosu);
+  double sin2u = (cosu + cosu) * sinu;
+  double cos2u = 1.0 - 2.0 * sinu * sinu;
+  temp = 1.0 / pl_safe;
+  double temp1 = 0.5 * j2 * temp;
+  double temp2 = temp1 * temp;
+
+  // short-period periodics  kernel.py:463-469
+  const double con41 = R.v[S_CON41], x1mth2 = R.v[S_X1MTH2];
+  double mrt = rl * (1.0 - 1.5 * temp2 * betal * con41) + 0.5 * temp1 * x1mth2 * cos2u;
+  su = su - 0.25 * temp2 * R.v[S_X7THM1] * sin2u;
+  double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
+  double xinc = R.v[S_INCLO] + 1.5 * temp2 * cosip * sinip * cos2u;
+  double mvt = rdotl - nm * temp1 * x1mth2 * sin2u / xke;
+  double rvdot = rvdotl + nm * temp1 * (x1mth2 * cos2u + 1.5 * con41) / xke;
+
+  // orientation  kernel.py:472-493
+  double sinsu, cossu, snod, cnod, sini, cosi;
+  sincos(su, &sinsu, &cossu);
+  sincos(xnode, &snod, &cnod);
+  sincos(xinc, &sini, &cosi);
+  double xmx = -snod * cosi;
+  double xmy = cnod * cosi;
+  double ux = xmx * sinsu + cnod * cossu;
+  double uy = xmy * sinsu + snod * cossu;
+  double uz = sini * sinsu;
+  double vx = xmx * cossu - cnod * sinsu;
+  double vy = xmy * cossu - snod * sinsu;
+  double vz = sini * cossu;
+  double mr = mrt * re;
+  o.r[0] = mr * ux;
+  o.r[1] = mr * uy;
+  o.r[2] = mr * uz;
+  o.v[0] = (mvt * ux + rvdot * vx) * vkmpersec;
+  o.v[1] = (mvt * uy + rvdot * vy) * vkmpersec;
+  o.v[2] = (mvt * uz + rvdot * vz) * vkmpersec;
+
+  // _first_error + init merge  kernel.py:495-502, 529-534
+  const bool decayed = mrt < 1.0;
+  int code = bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
+  int persistent = (flags >> CODE_SHIFT) & 0xff;
+  o.code = persistent != 0 ? persistent : code;
+}
+
+// ======================================================================
+// fp32 cell: the throughput path
+// ======================================================================
+struct Cell32 {
+  float r[3], v[3];
+  int code;
+};
+
+// x in radians -> reduced to about [-pi, pi] for accurate SFU evaluation.
+// p is the high word of rate*t, e collects every low-order term.
+__device__ __forceinline__ float reduce_df(float p, float e, float x0) {
+  float k = rintf(p * kInvTwoPiF);
+  float r = fmaf(-k, kTwoPiHiF, p);      // exact
+  r = fmaf(-k, kTwoPiLoF, r);
+  return r + (x0 + e);
+}
+
+// angle = x0 + (rate_hi + rate_lo) * (t_hi + t_lo), reduced mod 2*pi.
+__device__ __forceinline__ float secular_angle(float x0, float rate, float rate_lo, float th, float tl) {
+  float p = rate * th;
+  float e = fmaf(rate, th, -p);           // exact low part of rate*th
+  e = fmaf(rate, tl, e);
+  e = fmaf(rate_lo, th, e);
+  return reduce_df(p, e, x0);
+}
+
+// rotate (s, c) = (sin a, cos a) by a small angle d: sin(a + d), cos(a + d).
+// Series to d^3 / d^4: exact to < 1e-16 for |d| < 1e-3 (d is the J2
+// short-period correction, |d| <~ 1e-3 for pl >~ 1).
+__device__ __forceinline__ void rotate_small(float s, float c, float d, float& so, float& co) {
+  float d2 = d * d;
+  float sd = fmaf(d * d2, -1.0f / 6.0f, d);
+  float cd = fmaf(d2, -0.5f, 1.0f);
+  so = fmaf(s, cd, c * sd);
+  co = fmaf(c, cd, -s * sd);
+}
+
+__device__ __forceinline__ float frcp(float x) { return __frcp_rn(x); }
+
+__device__ __forceinline__ void cell32(const Rec<float>& R, float th, float tl, const Grav& g, Cell32& o) {
+  const float tiny = FLT_MIN;
+  const float xke = (float)g.xke, j2 = (float)g.j2, re = (float)g.re;
+  const float vkmpersec = (float)(g.re * g.xke / 60.0);
+  const float inv_xke = (float)(1.0 / g.xke);
+  const int flags = R.flags();
+  const bool isimp = flags & FLAG_ISIMP;
+  const float t = th + tl;
+
+  // secular gravity (double-float, reduced)  kernel.py:366-370
+  float xmdf = secular_angle(R.v[S_MO], R.v[S_MDOT], R.v[S_MDOT_LO], th, tl);
+  float argpdf = secular_angle(R.v[S_ARGPO], R.v[S_ARGPDOT], R.v[S_ARGPDOT_LO], th, tl);
+  float t2 = t * t;
+  float nodem = secular_angle(R.v[S_NODEO], R.v[S_NODEDOT], R.v[S_NODEDOT_LO], th, tl);
+  nodem = fmaf(R.v[S_NODECF], t2, nodem);
+  // u0 = mo + argpo and (mdot + argpdot) folded at init: the argument of
+  // Kepler's equation without its small terms (kernel.py:409-434).
+  float ubase = secular_angle(R.v[S_U0], R.v[S_UDOT], R.v[S_UDOT_LO], th, tl);
+
+  // drag  kernel.py:371-391
+  float tempa = fmaf(-R.v[S_CC1], t, 1.0f);
+  float tempe = R.v[S_BC4] * t;
+  float templ = R.v[S_T2COF] * t2;
+  float temp = 0.0f;
+  if (!isimp) {
+    float sx, cx;
+    __sincosf(xmdf, &sx, &cx);
+    float delmtemp = fmaf(R.v[S_ETA], cx, 1.0f);
+    float delm = R.v[S_XMCOF] * fmaf(delmtemp * delmtemp, delmtemp, -R.v[S_DELMO]);
+    temp = fmaf(R.v[S_OMGCOF], t, delm);
+    float t3 = t2 * t;
+    float t4 = t3 * t;
+    tempa = tempa - R.v[S_D2] * t2 - R.v[S_D3] * t3 - R.v[S_D4] * t4;
+    // sin(xmdf + temp): temp is the small drag correction
+    float smm = fmaf(cx, temp, sx);
+    smm = fmaf(-0.5f * sx, temp * temp, smm);
+    tempe = fmaf(R.v[S_BC5], smm - R.v[S_SINMAO], tempe);
+    templ = templ + R.v[S_T3COF] * t3 + t4 * fmaf(t, R.v[S_T5COF], R.v[S_T4COF]);
+  }
+  float argpm = argpdf - temp;
+
+  // mean motion / eccentricity  kernel.py:397-408
+  const bool bad_nm = flags & FLAG_BAD_NM;
+  float am = R.v[S_AM0] * tempa * tempa;
+  am = gmaxf(am, tiny);
+  float rsam = rsqrtf(am);
+  float nm = xke * (rsam * rsam * rsam);
+  float em = R.v[S_ECCO] - tempe;
+  const bool bad_em = (em >= 1.0f) || (em < -0.001f);
+  em = em < 1.0e-6f ? 1.0e-6f : em;
+  float mlt = R.v[S_NO] * templ;      // mm += no_unkozai * templ
+
+  // long-period periodics  kernel.py:420-431
+  float sa, ca;
+  __sincosf(argpm, &sa, &ca);
+  float axnl = em * ca;
+  float pl_lp = gmaxf(am * fmaf(-em, em, 1.0f), tiny);
+  float ilp = frcp(pl_lp);
+  float aynl = fmaf(em, sa, ilp * R.v[S_AYCOF]);
+  // u = xl - nodep = mm + argpm + xlcof/pl * axnl (mod 2pi); the drag
+  // term `temp` cancels between mm and argpm.
+  float u = ubase + mlt + ilp * R.v[S_XLCOF] * axnl;
+
+  // Kepler: fixed, warp-uniform iteration count  kernel.py:325-349
+  const int kiter = (flags >> KEPLER_SHIFT) & 0xf;
+  float eo1 = u, s, c;
+  float tem5 = 0.0f;
+#pragma unroll 1
+  for (int it = 0; it < kiter; ++it) {
+    __sincosf(eo1, &s, &c);
+    float den = fmaf(-s, aynl, fmaf(-c, axnl, 1.0f));
+    float num = fmaf(axnl, s, fmaf(-aynl, c, u)) - eo1;
+    tem5 = num * frcp(den);
+    tem5 = fminf(fmaxf(tem5, -0.95f), 0.95f);
+    eo1 += tem5;
+  }
+  // sin/cos of the final iterate: rotate the last evaluation by the last
+  // (converged, tiny) step instead of another SFU round trip.
+  float sineo1, coseo1;
+  if (kiter > 0 && kiter <= 3) {
+    rotate_small(s, c, tem5, sineo1, coseo1);
+  } else {
+    __sincosf(eo1, &sineo1, &coseo1);
+  }
+
+  // short-period preliminaries  kernel.py:440-460
+  float ecose = fmaf(axnl, coseo1, aynl * sineo1);
+  float esine = fmaf(axnl, sineo1, -aynl * coseo1);
+  float el2 = fmaf(axnl, axnl, aynl * aynl);
+  float pl = am * (1.0f - el2);
+  const bool bad_pl = pl < 0.0f;
+  float pl_safe = gmaxf(pl, tiny);
+  float rl = am * (1.0f - ecose);
+  float rl_safe = rl == 0.0f ? tiny : rl;
+  float irl = frcp(rl_safe);
+  float rdotl = (am * rsam) * esine * irl;        // sqrt(am) = am * rsqrt(am)
+  float rspl = rsqrtf(pl_safe);
+  float rvdotl = (pl_safe * rspl) * irl;          // sqrt(pl)
+  float omel2 = gmaxf(1.0f - el2, tiny);
+  float betal = omel2 * rsqrtf(omel2);
+  float tq = esine * frcp(1.0f + betal);
+  // (sinu, cosu) up to the positive factor am/rl, normalised: replaces the
+  // atan2 of kernel.py:455 (only sin/cos of su are ever used)
+  float sn = sineo1 - aynl - axnl * tq;
+  float cs = coseo1 - axnl + aynl * tq;
+  float nrm = rsqrtf(fmaf(sn, sn, cs * cs));
+  float sinu = sn * nrm, cosu = cs * nrm;
+  float sin2u = (cosu + cosu) * sinu;
+  float cos2u = fmaf(-2.0f * sinu, sinu, 1.0f);
+  float ipl = rspl * rspl;
+  float temp1 = 0.5f * j2 * ipl;
+  float temp2 = temp1 * ipl;
+
+  // short-period periodics  kernel.py:463-469
+  const float con41 = R.v[S_CON41], x1mth2 = R.v[S_X1MTH2];
+  const float cosip = R.v[S_COSIO], sinip = R.v[S_SINIO];
+  float mrt = fmaf(rl, fmaf(-1.5f * temp2 * betal, con41, 1.0f), 0.5f * temp1 * x1mth2 * cos2u);
+  float dsu = -0.25f * temp2 * R.v[S_X7THM1] * sin2u;
+  float dnode = 1.5f * temp2 * cosip * sin2u;
+  float dinc = 1.5f * temp2 * cosip * sinip * cos2u;
+  float nmt = nm * temp1 * inv_xke;
+  float mvt = fmaf(-nmt * x1mth2, sin2u, rdotl);
+  float rvdot = fmaf(nmt, fmaf(x1mth2, cos2u, 1.5f * con41), rvdotl);
+
+  // orientation  kernel.py:472-493
+  float sinsu, cossu, snod, cnod, sini, cosi;
+  rotate_small(sinu, cosu, dsu, sinsu, cossu);
+  __sincosf(nodem + dnode, &snod, &cnod);
+  rotate_small(sinip, cosip, dinc, sini, cosi);
+  float xmx = -snod * cosi;
+  float xmy = cnod * cosi;
+  float ux = fmaf(xmx, sinsu, cnod * cossu);
+  float uy = fmaf(xmy, sinsu, snod * cossu);
+  float uz = sini * sinsu;
+  float vx = fmaf(xmx, cossu, -cnod * sinsu);
+  float vy = fmaf(xmy, cossu, -snod * sinsu);
+  float vz = sini * cossu;
+  float mr = mrt * re;
+  o.r[0] = mr * ux;
+  o.r[1] = mr * uy;
+  o.r[2] = mr * uz;
+  o.v[0] = fmaf(mvt, ux, rvdot * vx) * vkmpersec;
+  o.v[1] = fmaf(mvt, uy, rvdot * vy) * vkmpersec;
+  o.v[2] = fmaf(mvt, uz, rvdot * vz) * vkmpersec;
+
+  const bool decayed = mrt < 1.0f;
+  int code = bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
+  int persistent = (flags >> CODE_SHIFT) & 0xff;
+  o.code = persistent != 0 ? persistent : code;
+}
+
+// ======================================================================
+// Packing: SoA fp64 satrec -> packed record (per satellite, fp64 math)
+// ======================================================================
+__device__ __forceinline__ int kepler_iters_for(double ecco) {
+  // fp32 Newton from E0 = u: error e -> ~e^2/2 -> ~e^5/8 ... ; these
+  // counts reach fp32 resolution.
+  double e = fabs(ecco) + 0.01;     // margin for drag-driven growth of em
+  if (e < 0.06) return 2;
+  if (e < 0.25) return 3;
+  if (e < 0.5) return 5;
+  return 10;
+}
+
+// split x into a float hi word and the float nearest the remainder
+__device__ __forceinline__ void split_df(double x, float& hi, float& lo) {
+  hi = (float)x;
+  lo = (float)(x - (double)hi);
+}
+
+template <typename T>
+__device__ __forceinline__ void store_record(const double* f, int init_code, bool isimp,
+                                             const Grav& g, T* __restrict__ rec);
+
+__device__ __forceinline__ void record_values(const double* f, int init_code, bool isimp,
+                                              const Grav& g, double* out, int& flags) {
+  const double no = f[F_NO_UNKOZAI];
+  const bool bad_nm = no <= 0.0;
+  const double nm_safe = bad_nm ? 1.0e-4 : no;
+  out[S_MO] = f[F_MO];
+  out[S_MDOT] = f[F_MDOT];
+  out[S_ARGPO] = f[F_ARGPO];
+  out[S_ARGPDOT] = f[F_ARGPDOT];
+  out[S_NODEO] = f[F_NODEO];
+  out[S_NODEDOT] = f[F_NODEDOT];
+  out[S_NODECF] = f[F_NODECF];
+  out[S_CC1] = f[F_CC1];
+  out[S_BC4] = f[F_BSTAR] * f[F_CC4];
+  out[S_T2COF] = f[F_T2COF];
+  out[S_OMGCOF] = f[F_OMGCOF];
+  out[S_ETA] = f[F_ETA];
+  out[S_XMCOF] = f[F_XMCOF];
+  out[S_DELMO] = f[F_DELMO];
+  out[S_D2] = f[F_D2];
+  out[S_D3] = f[F_D3];
+  out[S_D4] = f[F_D4];
+  out[S_BC5] = f[F_BSTAR] * f[F_CC5];
+  out[S_SINMAO] = f[F_SINMAO];
+  out[S_T3COF] = f[F_T3COF];
+  out[S_T4COF] = f[F_T4COF];
+  out[S_T5COF] = f[F_T5COF];
+  out[S_NO] = no;
+  out[S_AM0] = pow(g.xke / nm_safe, kX2o3);
+  out[S_ECCO] = f[F_ECCO];
+  out[S_INCLO] = f[F_INCLO];
+  double si, ci;
+  sincos(f[F_INCLO], &si, &ci);
+  out[S_SINIO] = si;
+  out[S_COSIO] = ci;
+  out[S_AYCOF] = f[F_AYCOF];
+  out[S_XLCOF] = f[F_XLCOF];
+  out[S_CON41] = f[F_CON41];
+  out[S_X1MTH2] = f[F_X1MTH2];
+  out[S_X7THM1] = f[F_X7THM1];
+  out[S_FLAGS] = 0.0;
+  out[S_MDOT_LO] = 0.0;
+  out[S_ARGPDOT_LO] = 0.0;
+  out[S_NODEDOT_LO] = 0.0;
+  out[S_UDOT] = f[F_MDOT] + f[F_ARGPDOT];
+  out[S_UDOT_LO] = 0.0;
+  out[S_U0] = pymod_2pi(f[F_MO] + f[F_ARGPO]);
+  const int persistent = init_code == 6 ? 0 : init_code;   // kernel.py:532
+  flags = (isimp ? FLAG_ISIMP : 0) | (bad_nm ? FLAG_BAD_NM : 0) |
+          (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0xff) << CODE_SHIFT);
+}
+
+template <>
+__device__ __forceinline__ void store_record<double>(const double* f, int init_code, bool isimp,
+                                                     const Grav& g, double* __restrict__ rec) {
+  double v[S_COUNT];
+  int flags;
+  record_values(f, init_code, isimp, g, v, flags);
+  v[S_FLAGS] = __longlong_as_double((long long)flags);
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) rec[i] = v[i];
+}
+
+template <>
+__device__ __forceinline__ void store_record<float>(const double* f, int init_code, bool isimp,
+                                                    const Grav& g, float* __restrict__ rec) {
+  double v[S_COUNT];
+  int flags;
+  record_values(f, init_code, isimp, g, v, flags);
+  float o[S_COUNT];
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) o[i] = (float)v[i];
+  split_df(f[F_MDOT], o[S_MDOT], o[S_MDOT_LO]);
+  split_df(f[F_ARGPDOT], o[S_ARGPDOT], o[S_ARGPDOT_LO]);
+  split_df(f[F_NODEDOT], o[S_NODEDOT], o[S_NODEDOT_LO]);
+  split_df(v[S_UDOT], o[S_UDOT], o[S_UDOT_LO]);
+  o[S_FLAGS] = __int_as_float(flags);
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) rec[i] = o[i];
+}
+
+// ======================================================================
+// Init (kernel.py:154-322), fp64, one thread per satellite
+// ======================================================================
+__device__ void init_one(const double el[7], const Grav& g, double* f, int& code, bool& isimp_out) {
+  const double tiny = DBL_MIN;
+  const double xke = g.xke, j2 = g.j2, j3oj2 = g.j3oj2, j4 = g.j4, re = g.re;
+  const double no_kozai = el[0], ecco = el[1], inclo = el[2], nodeo = el[3];
+  const double argpo = el[4], mo = el[5], bstar = el[6];
+
+  const bool bad_n = no_kozai <= 0.0;                              // :177
+  const bool bad_e = (ecco >= 1.0) || (ecco < -0.001);             // :178
+  const double no_safe = bad_n ? 1.0e-4 : no_kozai;
+
+  const double eccsq = ecco * ecco;
+  const double omeosq = gmax(1.0 - eccsq, tiny);
+  const double rteosq = sqrt(omeosq);
+  const double cosio = cos(inclo);
+  const double cosio2 = cosio * cosio;
+
+  // un-Kozai  :187-193
+  const double ak = pow(xke / no_safe, kX2o3);
+  const double d1 = 0.75 * j2 * (3.0 * cosio2 - 1.0) / (rteosq * omeosq);
+  double del = d1 / (ak * ak);
+  const double adel = ak * (1.0 - del * del - del * (1.0 / 3.0 + 134.0 * del * del / 81.0));
+  del = d1 / (adel * adel);
+  const double no_unkozai = no_safe / (1.0 + del);
+  const bool deep_space = kTwoPi / no_unkozai >= 225.0;             // :195
+
+  const double ao = pow(xke / no_unkozai, kX2o3);
+  const double sinio = sin(inclo);
+  const double po = ao * omeosq;
+  const double con42 = 1.0 - 5.0 * cosio2;
+  const double con41 = -con42 - cosio2 - cosio2;
+  const double posq = gmax(po * po, tiny);
+  const double rp = ao * (1.0 - ecco);
+  const bool isimp = rp < 220.0 / re + 1.0;                        // :205
+  const double perige = (rp - 1.0) * re;
+
+  // s* and (q0-s)^4 by perigee  :209-221
+  const double ss = 78.0 / re + 1.0;
+  const double qzms2t = pow((120.0 - 78.0) / re, 4.0);
+  const bool low_perige = perige < 156.0;
+  const double sfour_low = perige < 98.0 ? 20.0 : perige - 78.0;
+  const double qzms24temp = (120.0 - sfour_low) / re;
+  const double qzms24 = low_perige ? pow(qzms24temp, 4.0) : qzms2t;
+  const double sfour = low_perige ? sfour_low / re + 1.0 : ss;
+
+  // drag coefficients and secular rates  :223-275
+  const double pinvsq = 1.0 / posq;
+  double denom_tsi = ao - sfour;
+  denom_tsi = denom_tsi == 0.0 ? tiny : denom_tsi;
+  const double tsi = 1.0 / denom_tsi;
+  const double eta = ao * ecco * tsi;
+  const double etasq = eta * eta;
+  const double eeta = ecco * eta;
+  const double psisq = gmax(fabs(1.0 - etasq), tiny);
+  const double coef = qzms24 * pow(tsi, 4.0);
+  const double coef1 = coef / pow(psisq, 3.5);
+  const double cc2 = coef1 * no_unkozai *
+      (ao * (1.0 + 1.5 * etasq + eeta * (4.0 + etasq)) +
+       0.375 * j2 * tsi / psisq * con41 * (8.0 + 3.0 * etasq * (8.0 + etasq)));
+  const double cc1 = bstar * cc2;
+  const bool ecc_small = ecco <= 1.0e-4;
+  const double ecco_guard = gmax(ecco, 1.0e-4);
+  const double cc3 = ecc_small ? 0.0 * ecco
+                               : -2.0 * coef * tsi * j3oj2 * no_unkozai * sinio / ecco_guard;
+  const double x1mth2 = 1.0 - cosio2;
+  const double cc4 = 2.0 * no_unkozai * coef1 * ao * omeosq *
+      (eta * (2.0 + 0.5 * etasq) + ecco * (0.5 + 2.0 * etasq) -
+       j2 * tsi / (ao * psisq) *
+           (-3.0 * con41 * (1.0 - 2.0 * eeta + etasq * (1.5 - 0.5 * eeta)) +
+            0.75 * x1mth2 * (2.0 * etasq - eeta * (1.0 + etasq)) * cos(2.0 * argpo)));
+  const double cc5 = 2.0 * coef1 * ao * omeosq * (1.0 + 2.75 * (etasq + eeta) + eeta * etasq);
+  const double cosio4 = cosio2 * cosio2;
+  const double temp1 = 1.5 * j2 * pinvsq * no_unkozai;
+  const double temp2 = 0.5 * temp1 * j2 * pinvsq;
+  const double temp3 = -0.46875 * j4 * pinvsq * pinvsq * no_unkozai;
+  const double mdot = no_unkozai + 0.5 * temp1 * rteosq * con41 +
+                      0.0625 * temp2 * rteosq * (13.0 - 78.0 * cosio2 + 137.0 * cosio4);
+  const double argpdot = -0.5 * temp1 * con42 +
+                         0.0625 * temp2 * (7.0 - 114.0 * cosio2 + 395.0 * cosio4) +
+                         temp3 * (3.0 - 36.0 * cosio2 + 49.0 * cosio4);
+  const double xhdot1 = -temp1 * cosio;
+  const double nodedot = xhdot1 + (0.5 * temp2 * (4.0 - 19.0 * cosio2) +
+                                   2.0 * temp3 * (3.0 - 7.0 * cosio2)) * cosio;
+  const double omgcof = bstar * cc3 * cos(argpo);
+  const double eeta_guard = fabs(eeta) < tiny ? tiny : eeta;
+  const double xmcof = ecc_small ? 0.0 * ecco : -kX2o3 * coef * bstar / eeta_guard;
+  const double nodecf = 3.5 * omeosq * xhdot1 * cc1;
+  const double t2cof = 1.5 * cc1;
+  const double xlcof_den = fabs(cosio + 1.0) > 1.5e-12 ? 1.0 + cosio : 1.5e-12;
+  const double xlcof = -0.25 * j3oj2 * sinio * (3.0 + 5.0 * cosio) / xlcof_den;
+  const double aycof = -0.5 * j3oj2 * sinio;
+  const double delmotemp = 1.0 + eta * cos(mo);
+  const double delmo = delmotemp * delmotemp * delmotemp;
+  const double sinmao = sin(mo);
+  const double x7thm1 = 7.0 * cosio2 - 1.0;
+
+  // higher-order drag, zero in simplified mode  :278-294
+  const double cc1sq = cc1 * cc1;
+  double d2 = 4.0 * ao * tsi * cc1sq;
+  const double temp_d = d2 * tsi * cc1 / 3.0;
+  double d3 = (17.0 * ao + sfour) * temp_d;
+  double d4 = 0.5 * temp_d * ao * tsi * (221.0 * ao + 31.0 * sfour) * cc1;
+  double t3cof = d2 + 2.0 * cc1sq;
+  double t4cof = 0.25 * (3.0 * d3 + cc1 * (12.0 * d2 + 10.0 * cc1sq));
+  double t5cof = 0.2 * (3.0 * d4 + 12.0 * cc1 * d3 + 6.0 * d2 * d2 + 15.0 * cc1sq * (2.0 * d2 + cc1sq));
+  if (isimp) {
+    const double z = 0.0 * cc1;
+    d2 = z; d3 = z; d4 = z; t3cof = z; t4cof = z; t5cof = z;
+  }
+
+  f[F_NO_KOZAI] = no_kozai; f[F_ECCO] = ecco; f[F_INCLO] = inclo; f[F_NODEO] = nodeo;
+  f[F_ARGPO] = argpo; f[F_MO] = mo; f[F_BSTAR] = bstar;
+  f[F_NO_UNKOZAI] = no_unkozai; f[F_AO] = ao; f[F_CON41] = con41; f[F_X1MTH2] = x1mth2;
+  f[F_X7THM1] = x7thm1; f[F_MDOT] = mdot; f[F_ARGPDOT] = argpdot; f[F_NODEDOT] = nodedot;
+  f[F_NODECF] = nodecf; f[F_CC1] = cc1; f[F_CC4] = cc4; f[F_CC5] = cc5;
+  f[F_D2] = d2; f[F_D3] = d3; f[F_D4] = d4; f[F_T2COF] = t2cof; f[F_T3COF] = t3cof;
+  f[F_T4COF] = t4cof; f[F_T5COF] = t5cof; f[F_ETA] = eta; f[F_OMGCOF] = omgcof;
+  f[F_XMCOF] = xmcof; f[F_DELMO] = delmo; f[F_SINMAO] = sinmao; f[F_AYCOF] = aycof;
+  f[F_XLCOF] = xlcof;
+
+  // _first_error 2 > 1 > 7  :296-300
+  code = bad_n ? 2 : bad_e ? 1 : deep_space ? 7 : 0;
+  isimp_out = isimp;
+
+  // epoch evaluation  :316-322
+  Rec<double> R;
+  int flags;
+  record_values(f, 0, isimp, g, R.v, flags);
+  R.v[S_FLAGS] = __longlong_as_double((long long)flags);
+  Cell64 c0;
+  cell64(R, 0.0, g, c0);
+  if (code == 0) code = c0.code;
+}
+
+__global__ void init_kernel(const double* __restrict__ el, int64_t n, Grav g,
+                            double* __restrict__ satrec, int32_t* __restrict__ codes,
+                            uint8_t* __restrict__ isimp, void* __restrict__ rec, int precision) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double e[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) e[k] = el[k * n + i];
+  double f[F_COUNT];
+  int code;
+  bool simp;
+  init_one(e, g, f, code, simp);
+#pragma unroll
+  for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
+  codes[i] = code;
+  isimp[i] = simp ? 1 : 0;
+  if (rec != nullptr) {
+    if (precision == 64)
+      store_record<double>(f, code, simp, g, static_cast<double*>(rec) + i * S_COUNT);
+    else
+      store_record<float>(f, code, simp, g, static_cast<float*>(rec) + i * S_COUNT);
+  }
+}
+
+__global__ void pack_kernel(const double* __restrict__ satrec, const int32_t* __restrict__ codes,
+                            const uint8_t* __restrict__ isimp, int64_t n, Grav g,
+                            void* __restrict__ rec, int precision) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double f[F_COUNT];
+#pragma unroll
+  for (int k = 0; k < F_COUNT; ++k) f[k] = satrec[k * n + i];
+  if (precision == 64)
+    store_record<double>(f, codes[i], isimp[i] != 0, g, static_cast<double*>(rec) + i * S_COUNT);
+  else
+    store_record<float>(f, codes[i], isimp[i] != 0, g, static_cast<float*>(rec) + i * S_COUNT);
+}
+
+// ======================================================================
+// Propagate: dense grid
+// ======================================================================
+constexpr int kCellsPerLane = 4;
+constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // 128 time steps
+constexpr int kGridBlock = 256;
+
+__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(int32_t* p, int32_t v) { __stcs(reinterpret_cast<int*>(p), (int)v); }
+
+__device__ __forceinline__ void st_cs4(float* p, const float (&v)[4]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void st_cs4(double* p, const double (&v)[4]) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+  __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3]));
+}
+__device__ __forceinline__ void st_cs4(int32_t* p, const int (&v)[4]) {
+  __stcs(reinterpret_cast<int4*>(p), make_int4(v[0], v[1], v[2], v[3]));
+}
+
+template <typename T>
+struct CellT;
+template <>
+struct CellT<float> { using type = Cell32; };
+template <>
+struct CellT<double> { using type = Cell64; };
+
+__device__ __forceinline__ void eval(const Rec<float>& R, float th, float tl, const Grav& g, Cell32& c) {
+  cell32(R, th, tl, g, c);
+}
+__device__ __forceinline__ void eval(const Rec<double>& R, double th, float, const Grav& g, Cell64& c) {
+  cell64(R, th, g, c);
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kGridBlock)
+grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
+            const float* __restrict__ times_lo, int64_t m, Grav g, T* __restrict__ planes,
+            int64_t plane_stride, int64_t row_stride, int32_t* __restrict__ codes,
+            int64_t code_stride, int64_t chunks) {
+  const int64_t warp = ((int64_t)blockIdx.x * kGridBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t sat = warp / chunks;
+  if (sat >= n) return;
+  const int64_t chunk = warp - sat * chunks;
+  const int64_t j0 = chunk * kCellsPerWarp + lane * kCellsPerLane;
+  if (j0 >= m) return;
+
+  Rec<T> R;
+  load_rec(rec + sat * S_COUNT, R);
+
+  T th[kCellsPerLane];
+  float tl[kCellsPerLane];
+  const bool full = j0 + kCellsPerLane <= m;
+  if (VEC && full) {
+    if constexpr (sizeof(T) == 4) {
+      float4 q = __ldg(reinterpret_cast<const float4*>(times + j0));
+      th[0] = q.x; th[1] = q.y; th[2] = q.z; th[3] = q.w;
+    } else {
+      double2 a = __ldg(reinterpret_cast<const double2*>(times + j0));
+      double2 b = __ldg(reinterpret_cast<const double2*>(times + j0) + 1);
+      th[0] = a.x; th[1] = a.y; th[2] = b.x; th[3] = b.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
+  }
+#pragma unroll
+  for (int k = 0; k < kCellsPerLane; ++k)
+    tl[k] = (times_lo != nullptr && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
+
+  T out[6][kCellsPerLane];
+  int code[kCellsPerLane];
+#pragma unroll
+  for (int k = 0; k < kCellsPerLane; ++k) {
+    typename CellT<T>::type c;
+    eval(R, th[k], tl[k], g, c);
+    out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
+    out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
+    code[k] = c.code;
+  }
+
+  T* base = planes + sat * row_stride + j0;
+  int32_t* cbase = codes + sat * code_stride + j0;
+  if (VEC && full) {
+#pragma unroll
+    for (int p = 0; p < 6; ++p) st_cs4(base + p * plane_stride, out[p]);
+    st_cs4(cbase, code);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) {
+      if (j0 + k < m) {
+#pragma unroll
+        for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
+        st_cs(cbase + k, code[k]);
+      }
+    }
+  }
+}
+
+// ======================================================================
+// Propagate: elementwise pairs (broadcasting sgp4_propagate)
+// ======================================================================
+template <typename T>
+__global__ void __launch_bounds__(256)
+pairs_kernel(const T* __restrict__ rec, const int64_t* __restrict__ idx, const T* __restrict__ times,
+             const float* __restrict__ times_lo, int64_t p, Grav g, T* __restrict__ rv,
+             int32_t* __restrict__ codes) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  Rec<T> R;
+  load_rec(rec + idx[k] * S_COUNT, R);
+  typename CellT<T>::type c;
+  eval(R, times[k], times_lo != nullptr ? times_lo[k] : 0.0f, g, c);
+  rv[0 * p + k] = c.r[0]; rv[1 * p + k] = c.r[1]; rv[2 * p + k] = c.r[2];
+  rv[3 * p + k] = c.v[0]; rv[4 * p + k] = c.v[1]; rv[5 * p + k] = c.v[2];
+  codes[k] = c.code;
+}
+
+template <typename T>
+__global__ void kepler_kernel(const T* __restrict__ axnl, const T* __restrict__ aynl,
+                              const T* __restrict__ u, int64_t n, T* __restrict__ out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = kepler_reference<T>(axnl[k], aynl[k], u[k]);
+}
+
+bool grav_from(const double* grav, Grav& g) {
+  if (grav == nullptr) return false;
+  g.mu = grav[0]; g.re = grav[1]; g.xke = grav[2]; g.tumin = grav[3];
+  g.j2 = grav[4]; g.j3 = grav[5]; g.j4 = grav[6]; g.j3oj2 = grav[7];
+  return true;
+}
+
+inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+int sgp4b_abi_version(void) { return 1; }
+
+const char* sgp4b_last_error(void) { return g_last_error; }
+
+int sgp4b_init(const double* elements_dev, int64_t n, const double* grav, int precision,
+               double* satrec_dev, int32_t* init_code_dev, uint8_t* isimp_dev, void* record_dev,
+               void* stream) {
+  Grav g;
+  if (n <= 0) return fail(SGP4B_EINVAL, "sgp4b_init: n must be positive (got %lld)", (long long)n);
+  if (precision != 32 && precision != 64)
+    return fail(SGP4B_EINVAL, "sgp4b_init: precision must be 32 or 64, got %d", precision);
+  if (!elements_dev || !satrec_dev || !init_code_dev || !isimp_dev || !grav_from(grav, g))
+    return fail(SGP4B_EINVAL, "sgp4b_init: null pointer argument");
+  init_kernel<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      elements_dev, n, g, satrec_dev, init_code_dev, isimp_dev, record_dev, precision);
+  return check_launch("sgp4b_init");
+}
+
+int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev, const uint8_t* isimp_dev,
+               int64_t n, const double* grav, int precision, void* record_dev, void* stream) {
+  Grav g;
+  if (n <= 0) return fail(SGP4B_EINVAL, "sgp4b_pack: n must be positive");
+  if (precision != 32 && precision != 64)
+    return fail(SGP4B_EINVAL, "sgp4b_pack: precision must be 32 or 64, got %d", precision);
+  if (!satrec_dev || !init_code_dev || !isimp_dev || !record_dev || !grav_from(grav, g))
+    return fail(SGP4B_EINVAL, "sgp4b_pack: null pointer argument");
+  pack_kernel<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      satrec_dev, init_code_dev, isimp_dev, n, g, record_dev, precision);
+  return check_launch("sgp4b_pack");
+}
+
+int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_dev,
+                         const float* times_lo_dev, int64_t m, int precision, const double* grav,
+                         void* planes_dev, int64_t plane_stride, int64_t row_stride,
+                         int32_t* codes_dev, int64_t code_stride, void* stream) {
+  Grav g;
+  if (n <= 0 || m <= 0)
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: empty grid (%lld x %lld)", (long long)n,
+                (long long)m);
+  if (precision != 32 && precision != 64)
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: precision must be 32 or 64, got %d", precision);
+  if (!record_dev || !times_dev || !planes_dev || !codes_dev || !grav_from(grav, g))
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: null pointer argument");
+  if (row_stride < m || code_stride < m || plane_stride < (n - 1) * row_stride + m)
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: strides overlap the grid");
+  const size_t esz = precision == 64 ? 8 : 4;
+  const bool vec = (plane_stride % 4 == 0) && (row_stride % 4 == 0) && (code_stride % 4 == 0) &&
+                   ((uintptr_t)planes_dev % (4 * esz) == 0) && ((uintptr_t)codes_dev % 16 == 0) &&
+                   ((uintptr_t)times_dev % (4 * esz) == 0);
+  const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
+  const int64_t warps = n * chunks;
+  const int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
+  if (blocks > 0x7fffffffLL) return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: grid too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == 64) {
+    const double* rec = static_cast<const double*>(record_dev);
+    const double* t = static_cast<const double*>(times_dev);
+    double* out = static_cast<double*>(planes_dev);
+    if (vec)
+      grid_kernel<double, true><<<(unsigned)blocks, kGridBlock, 0, s>>>(
+          rec, n, t, nullptr, m, g, out, plane_stride, row_stride, codes_dev, code_stride, chunks);
+    else
+      grid_kernel<double, false><<<(unsigned)blocks, kGridBlock, 0, s>>>(
+          rec, n, t, nullptr, m, g, out, plane_stride, row_stride, codes_dev, code_stride, chunks);
+  } else {
+    const float* rec = static_cast<const float*>(record_dev);
+    const float* t = static_cast<const float*>(times_dev);
+    float* out = static_cast<float*>(planes_dev);
+    if (vec)
+      grid_kernel<float, true><<<(unsigned)blocks, kGridBlock, 0, s>>>(
+          rec, n, t, times_lo_dev, m, g, out, plane_stride, row_stride, codes_dev, code_stride,
+          chunks);
+    else
+      grid_kernel<float, false><<<(unsigned)blocks, kGridBlock, 0, s>>>(
+          rec, n, t, times_lo_dev, m, g, out, plane_stride, row_stride, codes_dev, code_stride,
+          chunks);
+  }
+  return check_launch("sgp4b_propagate_grid");
+}
+
+int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, const void* times_dev,
+                          const float* times_lo_dev, int64_t p, int precision, const double* grav,
+                          void* rv_dev, int32_t* codes_dev, void* stream) {
+  Grav g;
+  if (p <= 0) return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: p must be positive");
+  if (precision != 32 && precision != 64)
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: precision must be 32 or 64, got %d", precision);
+  if (!record_dev || !sat_idx_dev || !times_dev || !rv_dev || !codes_dev || !grav_from(grav, g))
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: null pointer argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == 64)
+    pairs_kernel<double><<<blocks_for(p, 256), 256, 0, s>>>(
+        static_cast<const double*>(record_dev), sat_idx_dev, static_cast<const double*>(times_dev),
+        nullptr, p, g, static_cast<double*>(rv_dev), codes_dev);
+  else
+    pairs_kernel<float><<<blocks_for(p, 256), 256, 0, s>>>(
+        static_cast<const float*>(record_dev), sat_idx_dev, static_cast<const float*>(times_dev),
+        times_lo_dev, p, g, static_cast<float*>(rv_dev), codes_dev);
+  return check_launch("sgp4b_propagate_pairs");
+}
+
+int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev, const void* u_dev, int64_t n,
+                       int precision, void* out_dev, void* stream) {
+  if (n <= 0) return fail(SGP4B_EINVAL, "sgp4b_solve_kepler: n must be positive");
+  if (precision != 32 && precision != 64)
+    return fail(SGP4B_EINVAL, "sgp4b_solve_kepler: precision must be 32 or 64, got %d", precision);
+  if (!axnl_dev || !aynl_dev || !u_dev || !out_dev)
+    return fail(SGP4B_EINVAL, "sgp4b_solve_kepler: null pointer argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == 64)
+    kepler_kernel<double><<<blocks_for(n, 256), 256, 0, s>>>(
+        static_cast<const double*>(axnl_dev), static_cast<const double*>(aynl_dev),
+        static_cast<const double*>(u_dev), n, static_cast<double*>(out_dev));
+  else
+    kepler_kernel<float><<<blocks_for(n, 256), 256, 0, s>>>(
+        static_cast<const float*>(axnl_dev), static_cast<const float*>(aynl_dev),
+        static_cast<const float*>(u_dev), n, static_cast<float*>(out_dev));
+  return check_launch("sgp4b_solve_kepler");
+}
+
+}  // extern "C"

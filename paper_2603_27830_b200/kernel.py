@@ -1,0 +1,227 @@
+"""Scalar / broadcasting SGP4 API (mirror of sgp4kit.kernel, kernel.py:45-558).
+
+``sgp4_init`` and ``sgp4_propagate`` keep the reference's signatures,
+dataclasses and broadcasting rules, but both run on the GPU through
+libsgp4b.so: init is the fp64 init kernel, propagate is the pairs kernel,
+which evaluates exactly the same cell function as the dense-grid kernel
+behind ``propagate_batch`` — so a batch cell equals the scalar call at the
+same precision bit for bit (the reference's batch≡scalar contract,
+tests/test_batch.py:39-64).
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, fields as dataclass_fields
+from typing import Any
+
+import numpy as np
+import torch
+
+from . import _device
+from .gravity import WGS72, GravityModel
+from .tle import ELEMENT_COLUMNS, MeanElements
+
+TWOPI = 2.0 * np.pi
+KEPLER_MAX_ITER = 10
+KEPLER_TOL = 1.0e-12
+KEPLER_CLAMP = 0.95
+DEEP_SPACE_PERIOD_MIN = 225.0
+
+
+class ErrorCode(enum.IntEnum):
+    """Per-cell status codes (kernel.py:45-52); 3 is declared, never produced."""
+
+    OK = 0
+    ECC_OUT_OF_RANGE = 1
+    MEAN_MOTION_NONPOSITIVE = 2
+    PERT_ECC_OUT_OF_RANGE = 3
+    SEMILATUS_NEGATIVE = 4
+    SUBORBITAL = 6
+    DEEP_SPACE_UNSUPPORTED = 7
+
+
+#: SatInit float fields in the order of the device SoA satrec (33 columns)
+SATREC_FIELD_NAMES = (
+    "no_kozai", "ecco", "inclo", "nodeo", "argpo", "mo", "bstar",
+    "no_unkozai", "ao", "con41", "x1mth2", "x7thm1",
+    "mdot", "argpdot", "nodedot", "nodecf",
+    "cc1", "cc4", "cc5", "d2", "d3", "d4", "t2cof", "t3cof", "t4cof", "t5cof",
+    "eta", "omgcof", "xmcof", "delmo", "sinmao", "aycof", "xlcof",
+)
+assert len(SATREC_FIELD_NAMES) == _device.SATREC_FIELDS
+
+
+@dataclass(frozen=True)
+class SatInit:
+    """Initialisation constants (kernel.py:55-109), scalars or parallel arrays.
+
+    An instance produced by :func:`sgp4_init` / ``init_batch`` also carries
+    (as a non-field attribute) the GPU-resident packed records it was built
+    from; an instance built or edited by hand is re-packed on the GPU on
+    first use.
+    """
+
+    grav: GravityModel
+    dtype: Any
+    no_kozai: Any
+    ecco: Any
+    inclo: Any
+    nodeo: Any
+    argpo: Any
+    mo: Any
+    bstar: Any
+    no_unkozai: Any
+    ao: Any
+    con41: Any
+    x1mth2: Any
+    x7thm1: Any
+    mdot: Any
+    argpdot: Any
+    nodedot: Any
+    nodecf: Any
+    isimp: Any
+    cc1: Any
+    cc4: Any
+    cc5: Any
+    d2: Any
+    d3: Any
+    d4: Any
+    t2cof: Any
+    t3cof: Any
+    t4cof: Any
+    t5cof: Any
+    eta: Any
+    omgcof: Any
+    xmcof: Any
+    delmo: Any
+    sinmao: Any
+    aycof: Any
+    xlcof: Any
+    error_code_at_init: Any
+
+
+@dataclass(frozen=True)
+class StateVector:
+    """TEME position (km) and velocity (km/s) plus the int32 status."""
+
+    r: Any
+    v: Any
+    error_code: Any
+
+
+def satinit_from_device(dev: "_device.DeviceSatrec", shape: tuple) -> SatInit:
+    """Materialise the public SatInit (host numpy) from a device satrec."""
+    dtype = _device.np_dtype(dev.precision)
+    sr = dev.satrec.cpu().numpy()
+    values = {name: sr[k].astype(dtype).reshape(shape)
+              for k, name in enumerate(SATREC_FIELD_NAMES)}
+    values["isimp"] = dev.isimp.cpu().numpy().astype(bool).reshape(shape)
+    values["error_code_at_init"] = dev.codes.cpu().numpy().astype(np.int32).reshape(shape)
+    init = SatInit(grav=dev.grav, dtype=dtype, **values)
+    object.__setattr__(init, "_sgp4b_dev", dev)
+    object.__setattr__(init, "_sgp4b_shape", tuple(shape))
+    return init
+
+
+def _element_columns(elems: MeanElements) -> tuple[np.ndarray, tuple]:
+    arrays = [np.asarray(getattr(elems, name), dtype=np.float64) for name in ELEMENT_COLUMNS]
+    shape = np.broadcast_shapes(*(a.shape for a in arrays))
+    cols = np.stack([np.broadcast_to(a, shape).ravel() for a in arrays])
+    return cols, shape
+
+
+def sgp4_init(elems: MeanElements, grav: GravityModel = WGS72,
+              dtype=np.float64) -> SatInit:
+    """All propagation constants from canonical mean elements (kernel.py:139).
+
+    Runs the fp64 init kernel (including the epoch evaluation that flags
+    immediate decay) and rounds the constants to ``dtype``.  Never raises on
+    anomalous elements: ``error_code_at_init`` is non-zero instead.
+    """
+    precision = _device.precision_of(dtype)
+    cols, shape = _element_columns(elems)
+    if cols.shape[1] == 0:
+        raise ValueError("empty element arrays")
+    dev = _device.init_device(cols, grav, precision)
+    return satinit_from_device(dev, shape)
+
+
+def _device_of(init: SatInit) -> tuple["_device.DeviceSatrec", tuple]:
+    """The packed GPU records behind ``init`` (re-packed if hand-built)."""
+    dev = getattr(init, "_sgp4b_dev", None)
+    if dev is not None:
+        return dev, init._sgp4b_shape
+    precision = _device.precision_of(init.dtype)
+    arrays = [np.asarray(getattr(init, name), dtype=np.float64) for name in SATREC_FIELD_NAMES]
+    isimp = np.asarray(init.isimp)
+    codes = np.asarray(init.error_code_at_init)
+    shape = np.broadcast_shapes(*(a.shape for a in arrays), isimp.shape, codes.shape)
+    sr = np.stack([np.broadcast_to(a, shape).ravel() for a in arrays])
+    dev = _device.pack_device(sr, np.broadcast_to(codes, shape).ravel(),
+                              np.broadcast_to(isimp, shape).ravel(), init.grav, precision)
+    object.__setattr__(init, "_sgp4b_dev", dev)
+    object.__setattr__(init, "_sgp4b_shape", tuple(shape))
+    return dev, tuple(shape)
+
+
+def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
+    """Propagate to ``tsince_min`` minutes since epoch (kernel.py:513-534).
+
+    Broadcasts the satellite shape of ``init`` against the time shape; scalar
+    in, scalar out; r/v have a trailing axis of 3.  Times are cast to the
+    init dtype first, as in the reference.
+    """
+    dtype = np.dtype(init.dtype)
+    t = np.asarray(tsince_min, dtype=dtype)
+    dev, sat_shape = _device_of(init)
+    out_shape = np.broadcast_shapes(sat_shape, t.shape)
+    p = int(np.prod(out_shape, dtype=np.int64))
+    r = np.empty(out_shape + (3,), dtype=dtype)
+    v = np.empty(out_shape + (3,), dtype=dtype)
+    if p == 0:
+        return StateVector(r=r, v=v, error_code=np.zeros(out_shape, dtype=np.int32))
+    idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape), out_shape).ravel()
+    tt = np.ascontiguousarray(np.broadcast_to(t, out_shape).ravel())
+    device = dev.device
+    with torch.cuda.device(device):
+        idx_d = torch.from_numpy(np.ascontiguousarray(idx)).to(device)
+        t_d = torch.from_numpy(tt).to(device)
+        rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
+        codes = torch.empty((p,), dtype=torch.int32, device=device)
+        _device.propagate_pairs(dev, idx_d, t_d, rv, codes)
+        rv_h = rv.cpu().numpy()
+        codes_h = codes.cpu().numpy()
+    r[...] = rv_h[:3].T.reshape(out_shape + (3,))
+    v[...] = rv_h[3:].T.reshape(out_shape + (3,))
+    return StateVector(r=r, v=v, error_code=codes_h.reshape(out_shape))
+
+
+def solve_kepler(axnl, aynl, u_init):
+    """Newton solve of SGP4's Kepler equation (kernel.py:325-349): at most 10
+    steps, step clamped to ±0.95, per-element freeze once |step| < 1e-12."""
+    a, b, u = np.broadcast_arrays(np.asarray(axnl), np.asarray(aynl), np.asarray(u_init))
+    dtype = np.result_type(a, b, u)
+    if dtype not in (np.float32, np.float64):
+        dtype = np.float64
+    precision = _device.precision_of(dtype)
+    device = _device.require_cuda()
+    tens = [torch.from_numpy(np.ascontiguousarray(x, dtype=dtype).ravel()).to(device)
+            for x in (a, b, u)]
+    if tens[0].numel() == 0:
+        return np.empty(a.shape, dtype=dtype)
+    out = _device.solve_kepler_device(*tens, precision).cpu().numpy().reshape(a.shape)
+    return out if out.ndim else out[()]
+
+
+_DAYS_BEFORE = (0, 31, 59, 90, 120, 151, 181, 212, 243, 273, 304, 334)
+
+
+def epoch_to_julian(epoch_year: int, epoch_day_int: int, epoch_day_frac: float) -> float:
+    """Julian date of a split TLE epoch, fp64 host arithmetic (kernel.py:544-558)."""
+    leap = epoch_year % 4 == 0 and (epoch_year % 100 != 0 or epoch_year % 400 == 0)
+    if not 1 <= epoch_day_int <= (366 if leap else 365):
+        raise ValueError(f"day {epoch_day_int} out of range for year {epoch_year}")
+    y = epoch_year - 1
+    jan0 = 1721424.5 + 365 * y + y // 4 - y // 100 + y // 400
+    return jan0 + float(epoch_day_int) + float(epoch_day_frac)

@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA kernels (through the C ABI) against the CPU oracle,
+which is itself pinned bit-for-bit to the reference (test_oracle.py).
+
+Tolerances (BASELINE.json north_star):
+  fp64: |dr| <= 1 mm (1e-6 km), |dv| <= 1e-6 km/s, error codes bit-exact;
+  fp32: error codes bit-exact vs the reference at fp32 AND fp64; position /
+        velocity error vs the reference fp64 path is reported (and bounded
+        loosely so a regression cannot hide).
+"""
+
+import dataclasses
+import io
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL64_R = 1.0e-6     # km
+TOL64_V = 1.0e-6     # km/s
+
+
+def _gpu():
+    import paper_2603_27830_b200 as pkg
+    return pkg
+
+
+def _diff(planes, ref_planes, mask):
+    dr = np.linalg.norm((planes[:3].astype(np.float64) - ref_planes[:3])[:, mask], axis=0)
+    dv = np.linalg.norm((planes[3:].astype(np.float64) - ref_planes[3:])[:, mask], axis=0)
+    return dr, dv
+
+
+@pytest.fixture(scope="module")
+def corpus_ref64(oracle, corpus_columns):
+    times = np.linspace(0.0, 1440.0, 200)
+    sat = oracle.init_columns(corpus_columns, 64)
+    return times, oracle.grid(sat, times, workers=4)
+
+
+@pytest.mark.parametrize("times_kind", ["day", "fortnight"])
+def test_fp64_corpus_parity(oracle, corpus_columns, corpus_ref64, times_kind):
+    pkg = _gpu()
+    if times_kind == "day":
+        times, (ref_planes, ref_codes) = corpus_ref64
+    else:
+        times = np.arange(0.0, 20160.0, 101.0)
+        ref_planes, ref_codes = oracle.grid(oracle.init_columns(corpus_columns, 64), times,
+                                            workers=4)
+    res = pkg.propagate_batch(pkg.init_batch(corpus_columns, precision=64), times)
+    assert res.planes.dtype == np.float64 and res.error.dtype == np.int32
+    assert np.array_equal(res.error, ref_codes)
+    ok = ref_codes == 0
+    dr, dv = _diff(res.planes, ref_planes, ok)
+    print(f"\nfp64 {times_kind}: {ok.sum()} ok cells, max|dr|={dr.max():.3e} km, "
+          f"max|dv|={dv.max():.3e} km/s, nonzero codes={int((~ok).sum())}")
+    assert dr.max() <= TOL64_R and dv.max() <= TOL64_V
+    assert np.isfinite(res.planes).all()
+
+
+def test_fp64_matches_reference_goldens(golden_columns, golden_states):
+    pkg = _gpu()
+    g = golden_states[64]
+    res = pkg.propagate_batch(pkg.init_batch(golden_columns, precision=64), g["times"])
+    assert np.array_equal(res.error, g["error"])
+    dr, dv = _diff(res.planes, g["planes"], g["error"] == 0)
+    assert dr.max() <= TOL64_R and dv.max() <= TOL64_V
+
+
+def test_fp32_codes_and_accuracy(oracle, corpus_columns, corpus_ref64):
+    pkg = _gpu()
+    times, (ref64, codes64) = corpus_ref64
+    _, codes32 = oracle.grid(oracle.init_columns(corpus_columns, 32), times, workers=4)
+    res = pkg.propagate_batch(pkg.init_batch(corpus_columns, precision=32), times)
+    assert res.planes.dtype == np.float32
+    assert np.array_equal(res.error, codes64)
+    assert np.array_equal(res.error, codes32)
+    ok = codes64 == 0
+    dr, dv = _diff(res.planes, ref64, ok)
+    print(f"\nfp32 vs reference fp64 (1,200 x 200, 1 day): |dr| median "
+          f"{np.median(dr) * 1e3:.2f} m p99 {np.percentile(dr, 99) * 1e3:.2f} m max "
+          f"{dr.max() * 1e3:.2f} m; |dv| max {dv.max() * 1e3:.4f} m/s")
+    assert np.median(dr) < 0.05 and dr.max() < 1.0 and dv.max() < 1e-3
+
+
+def test_fp32_goldens_codes(golden_columns, golden_states):
+    pkg = _gpu()
+    g = golden_states[32]
+    res = pkg.propagate_batch(pkg.init_batch(golden_columns, precision=32), g["times"])
+    assert np.array_equal(res.error, g["error"])
+    assert np.array_equal(res.error, golden_states[64]["error"])
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_failure_modes(failure_table, precision):
+    pkg = _gpu()
+    times = np.array(failure_table["times"])
+    cols = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    sats = pkg.init_batch(cols, precision=precision)
+    res = pkg.propagate_batch(sats, times)
+    for k, (key, row) in enumerate(failure_table["cases"].items()):
+        assert int(sats.error_codes[k]) == row[f"init_code_{precision}"], key
+        assert res.error[k].tolist() == row[f"codes_{precision}"], key
+        assert np.isfinite(res.planes[:, k]).all(), key
+
+
+def test_init_constants_vs_oracle(oracle, golden_columns, golden_states):
+    pkg = _gpu()
+    sats = pkg.init_batch(golden_columns, precision=64)
+    init = sats.init
+    ref = golden_states[64]
+    for name in oracle.SATREC_FIELDS:
+        np.testing.assert_allclose(np.asarray(getattr(init, name)), ref["init_" + name],
+                                   rtol=1e-12, atol=1e-300, err_msg=name)
+    assert np.array_equal(init.isimp, ref["init_isimp"])
+    assert np.array_equal(init.error_code_at_init, ref["init_error_code_at_init"])
+    init32 = pkg.init_batch(golden_columns, precision=32).init
+    assert init32.cc1.dtype == np.float32 and init32.dtype == np.float32
+
+
+@pytest.mark.parametrize("precision,dtype", [(64, np.float64), (32, np.float32)])
+def test_batch_equals_scalar_bitwise(real_elements, precision, dtype):
+    """tests/test_batch.py:39-64 of the reference: batch cell == scalar call."""
+    pkg = _gpu()
+    els = list(real_elements.values())
+    times = np.array([0.0, 30.0, 720.0, 1440.0, -60.0, 4321.5, 20160.0])
+    res = pkg.propagate_batch(pkg.init_batch(els, precision=precision), times)
+    for i, el in enumerate(els):
+        init = pkg.sgp4_init(el, dtype=dtype)
+        for j, t in enumerate(times):
+            s = pkg.sgp4_propagate(init, dtype(t))
+            assert np.asarray(s.r).dtype == dtype
+            assert np.array_equal(res.planes[:3, i, j], np.asarray(s.r))
+            assert np.array_equal(res.planes[3:, i, j], np.asarray(s.v))
+            assert res.error[i, j] == int(np.asarray(s.error_code))
+
+
+def test_scalar_broadcast_shapes(real_elements):
+    pkg = _gpu()
+    el = real_elements["ISS"]
+    init = pkg.sgp4_init(el)
+    s = pkg.sgp4_propagate(init, 60.0)
+    assert np.asarray(s.r).shape == (3,) and np.asarray(s.error_code).shape == ()
+    s = pkg.sgp4_propagate(init, np.array([0.0, 60.0, 120.0]))
+    assert s.r.shape == (3, 3) and s.error_code.shape == (3,)
+    # edited SatInit (dataclasses.replace) is re-packed on the GPU
+    edited = dataclasses.replace(init, bstar=np.asarray(init.bstar) * 2)
+    s2 = pkg.sgp4_propagate(edited, 60.0)
+    assert np.isfinite(s2.r).all()
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (2, 3), (33, 5), (7, 127), (5, 129), (3, 1001)])
+def test_odd_shapes_match_oracle(oracle, corpus_columns, n, m):
+    pkg = _gpu()
+    cols = corpus_columns[:, :n]
+    times = np.linspace(-100.0, 3000.0, m)
+    res = pkg.propagate_batch(pkg.init_batch(cols, precision=64), times)
+    ref_planes, ref_codes = oracle.grid(oracle.init_columns(cols, 64), times)
+    assert np.array_equal(res.error, ref_codes)
+    dr, dv = _diff(res.planes, ref_planes, ref_codes == 0)
+    assert dr.max(initial=0) <= TOL64_R and dv.max(initial=0) <= TOL64_V
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_row_shards_bitwise_equal_full_grid(corpus_columns, precision):
+    """Satellite sharding (one GPU per range, no collective) is bitwise
+    invariant — the analogue of reference worker invariance."""
+    import torch
+    from paper_2603_27830_b200 import _device
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :301], precision=precision)
+    times = np.linspace(0.0, 1440.0, 77)
+    full = pkg.propagate_batch_device(sats, times)
+    t_d = torch.from_numpy(times.astype(sats.dtype)).cuda()
+    for lo, hi in pkg.partition_work(301, 1, 4):
+        planes = torch.empty((6, hi - lo, 77), dtype=full.planes.dtype, device="cuda")
+        err = torch.empty((hi - lo, 77), dtype=torch.int32, device="cuda")
+        _device.propagate_grid(sats.device_satrec, t_d, planes, err, rows=(lo, hi))
+        assert torch.equal(planes, full.planes[:, lo:hi])
+        assert torch.equal(err, full.error[lo:hi])
+
+
+def test_streamed_tiles_match_dense(corpus_columns):
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :7])
+    times = np.linspace(0.0, 720.0, 9)
+    dense = pkg.propagate_batch(sats, times)
+    got = np.full_like(dense.planes, np.nan)
+    got_err = np.full_like(dense.error, -1)
+    seen = []
+
+    def sink(rows, cols, planes, error):
+        seen.append((rows.start, cols.start))
+        got[:, rows, cols] = planes
+        got_err[rows, cols] = error
+
+    summary = pkg.propagate_batch_streamed(sats, times, tile_rows=3, tile_cols=4, sink=sink)
+    assert seen == sorted(seen)
+    assert np.array_equal(got, dense.planes) and np.array_equal(got_err, dense.error)
+    assert summary.cells_emitted == 7 * 9
+    assert summary.nonzero_error_count == int(np.count_nonzero(dense.error))
+
+    calls = []
+
+    def failing(rows, cols, planes, error):
+        calls.append(1)
+        if len(calls) == 3:
+            raise IOError("disk full")
+
+    with pytest.raises(pkg.StreamAborted) as exc:
+        pkg.propagate_batch_streamed(pkg.init_batch(corpus_columns[:, :4]),
+                                     np.linspace(0.0, 720.0, 4), 1, 2, failing)
+    assert exc.value.tiles_completed == 2
+
+
+def test_sgb1_from_device_equals_host(corpus_columns):
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :3], precision=32)
+    times = np.array([0.0, 60.0, 120.0, 240.0, 480.0])
+    host = pkg.propagate_batch(sats, times)
+    dev = pkg.propagate_batch_device(sats, times)
+    a, b = io.BytesIO(), io.BytesIO()
+    pkg.write_grid_binary(host, a)
+    pkg.write_grid_binary(dev, b)
+    assert a.getvalue() == b.getvalue()
+    raw = a.getvalue()
+    assert raw[:4] == b"SGB1" and raw[24:32] == b"rrrvvve\x00"
+    back = pkg.read_grid_binary(io.BytesIO(raw))
+    assert np.array_equal(back.planes, host.planes) and np.array_equal(back.error, host.error)
+
+
+def test_validation_errors(corpus_columns):
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :1])
+    with pytest.raises(ValueError):
+        pkg.propagate_batch(sats, np.empty(0))
+    with pytest.raises(ValueError):
+        pkg.propagate_batch(sats, np.zeros((2, 2)))
+    with pytest.raises(ValueError):
+        pkg.init_batch([])
+    with pytest.raises(ValueError):
+        pkg.init_batch(corpus_columns[:, :1], precision=16)
+    with pytest.raises(pkg.GridAllocationError):
+        pkg.propagate_batch_device(pkg.init_batch(corpus_columns), np.zeros(10 ** 9))
+
+
+def test_solve_kepler_gpu():
+    import math
+    from paper_2603_27830_b200.kernel import solve_kepler
+    ax = np.array([0.1, 0.0, 0.02, 0.3])
+    ay = np.array([0.0, 0.05, 0.03, -0.2])
+    u = np.array([1.0, 2.5, 5.9, 0.4])
+    e = solve_kepler(ax, ay, u)
+    res = u - (e - ax * np.sin(e) + ay * np.cos(e))
+    assert np.abs(res).max() < 1e-12
+    assert float(solve_kepler(np.float64(0), np.float64(0), np.float64(1.2345))) == 1.2345
+    singles = np.array([float(solve_kepler(a, b, c)) for a, b, c in zip(ax, ay, u)])
+    assert np.array_equal(singles, e)
+    assert math.isfinite(float(solve_kepler(np.float32(0.3), np.float32(0.2), np.float32(1.0))))
+
+
+def test_starlink_full_size_properties():
+    """C2 at full size (9,341 x 1,000): properties that need no oracle —
+    no error codes, finite, plausible LEO radii/speeds, fp32 close to fp64
+    on every cell — plus a 2,000-cell random sample checked against the
+    oracle."""
+    import torch
+    from oracle import sgp4_oracle as oracle
+    from paper_2603_27830_b200.catalog import starlink_like
+    pkg = _gpu()
+    cols = starlink_like(9341)
+    times = np.linspace(0.0, 1440.0, 1000)
+    r32 = pkg.propagate_batch_device(pkg.init_batch(cols, precision=32), times)
+    r64 = pkg.propagate_batch_device(pkg.init_batch(cols, precision=64), times)
+    assert int(torch.count_nonzero(r32.error)) == 0 and int(torch.count_nonzero(r64.error)) == 0
+    rad = torch.linalg.vector_norm(r64.planes[:3], dim=0)
+    spd = torch.linalg.vector_norm(r64.planes[3:], dim=0)
+    assert 6700 < float(rad.min()) and float(rad.max()) < 7000
+    assert 7.2 < float(spd.min()) and float(spd.max()) < 7.9
+    d = torch.linalg.vector_norm(r32.planes[:3].double() - r64.planes[:3], dim=0)
+    print(f"\nC2 fp32 vs GPU fp64: median {float(d.median()) * 1e3:.2f} m, "
+          f"max {float(d.max()) * 1e3:.2f} m")
+    assert float(d.max()) < 1.0
+    rng = np.random.default_rng(7)
+    ii = rng.integers(0, 9341, 2000)
+    jj = rng.integers(0, 1000, 2000)
+    sat = oracle.init_columns(cols[:, ii], 64)
+    ref_r, ref_v, ref_c = oracle.propagate_merged(sat, times[jj])
+    got = r64.planes[:, ii, jj].cpu().numpy()
+    assert (ref_c == 0).all()
+    assert np.abs(got[:3].T - ref_r).max() <= TOL64_R
+    assert np.abs(got[3:].T - ref_v).max() <= TOL64_V

@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench, launch list, ncu capture of the grid kernel.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu -s > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 600 python bench.py --precision 64 --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 5 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -s 3 -c 1 -o gpurun_out/prof_c2_fp32 python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -s 3 -c 1 -o gpurun_out/prof_c3_fp64 python bench.py --precision 64 --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_full64.log 2>&1
+ls -la gpurun_out
