@@ -39,6 +39,7 @@ namespace {
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 constexpr double kInvTwoPi = 0.15915494309189533576888376337251;
 constexpr double kX2o3 = 2.0 / 3.0;
+constexpr double kPi = 3.14159265358979323846264338327950;
 
 // 2*pi split for float Cody-Waite reduction: hi has 8 trailing zero bits so
 // k*hi is exact for |k| < 2^8 ... we rely on fmaf exactness instead (see
@@ -49,6 +50,9 @@ constexpr float kInvTwoPiF = 0.159154943091895335768883763372514f;
 
 struct Grav {
   double mu, re, xke, tumin, j2, j3, j4, j3oj2;
+  // derived on the host once per launch (propagate kernels)
+  double vkm;                                    // re * xke / 60
+  float xke_f, re_f, vkm_f, inv_xke_f, half_j2_f;
 };
 
 // ---- SoA satrec fields: SatInit float fields in dataclass order --------
@@ -75,6 +79,14 @@ enum Slot {
   S_COUNT
 };
 static_assert(S_COUNT == SGP4B_RECORD_SLOTS, "record slot count");
+
+// fp32 records re-purpose slots the fp32 cell does not read to hold
+// per-satellite products (computed in fp64 at pack time):
+constexpr int S32_NEG15CON41 = S_CON41;      // -1.5 con41
+constexpr int S32_HALFX1MTH2 = S_MDOT_LO;    //  0.5 x1mth2
+constexpr int S32_QX7THM1 = S_X7THM1;        // -0.25 x7thm1
+constexpr int S32_C15COSIO = S_ARGPDOT_LO;   //  1.5 cosio
+constexpr int S32_C15COSSIN = S_NODEDOT_LO;  //  1.5 cosio sinio
 
 // flags word
 constexpr int FLAG_ISIMP = 1;
@@ -106,7 +118,6 @@ int check_launch(const char* what) {
 
 // dmath.maximum(x, floor) == where(x >= floor, x, floor)   dmath.py:213-215
 __device__ __forceinline__ double gmax(double x, double f) { return x >= f ? x : f; }
-__device__ __forceinline__ float gmaxf(float x, float f) { return x >= f ? x : f; }
 
 // C fmod(x, 2*pi), exact: with the right integer quotient q the remainder
 // x - q*2pi is representable, so one fma produces it without rounding.
@@ -217,7 +228,7 @@ struct Cell64 {
 __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Grav& g, Cell64& o) {
   const double tiny = DBL_MIN;
   const double xke = g.xke, j2 = g.j2, re = g.re;
-  const double vkmpersec = re * xke / 60.0;
+  const double vkmpersec = g.vkm;
   const int flags = R.flags();
   const bool isimp = flags & FLAG_ISIMP;
 
@@ -346,27 +357,40 @@ struct Cell32 {
   int code;
 };
 
-// x in radians -> reduced to about [-pi, pi] for accurate SFU evaluation.
-// p is the high word of rate*t, e collects every low-order term.
-__device__ __forceinline__ float reduce_df(float p, float e, float x0) {
+// SFU (MUFU) approximations with flush-to-zero: one MUFU each (sin/cos add
+// the FMUL by 1/2pi the SFU expects).  Absolute error of sin/cos ~2^-21 on
+// [-pi, pi]; rcp/rsqrt ~1 ulp.
+__device__ __forceinline__ float rcp_a(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsq_a(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void sincos_a(float x, float& s, float& c) {
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(x));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(x));
+}
+
+// x0 + (rate_hi + rate_lo) * (t + tl), reduced mod 2*pi, in double-float:
+// p = rate_hi*t rounded, its exact error by fma, k = nearest revolution;
+// p - k*2pi_hi is exact (the difference needs < 24 bits: DESIGN.md §4).
+__device__ __forceinline__ float secular_angle(float x0, float rate, float rate_lo, float t, float tl) {
+  float p = rate * t;
+  float e = fmaf(rate, t, -p);
+  e = fmaf(rate_lo, t, e);
+  e = fmaf(rate, tl, e);
   float k = rintf(p * kInvTwoPiF);
-  float r = fmaf(-k, kTwoPiHiF, p);      // exact
+  float r = fmaf(-k, kTwoPiHiF, p);
   r = fmaf(-k, kTwoPiLoF, r);
   return r + (x0 + e);
 }
 
-// angle = x0 + (rate_hi + rate_lo) * (t_hi + t_lo), reduced mod 2*pi.
-__device__ __forceinline__ float secular_angle(float x0, float rate, float rate_lo, float th, float tl) {
-  float p = rate * th;
-  float e = fmaf(rate, th, -p);           // exact low part of rate*th
-  e = fmaf(rate, tl, e);
-  e = fmaf(rate_lo, th, e);
-  return reduce_df(p, e, x0);
-}
-
-// rotate (s, c) = (sin a, cos a) by a small angle d: sin(a + d), cos(a + d).
-// Series to d^3 / d^4: exact to < 1e-16 for |d| < 1e-3 (d is the J2
-// short-period correction, |d| <~ 1e-3 for pl >~ 1).
+// (sin, cos)(a + d) from (sin, cos)(a) for a small angle d (series to
+// d^3 / d^2; |d| < 1e-2 keeps the truncation below fp32 resolution).
 __device__ __forceinline__ void rotate_small(float s, float c, float d, float& so, float& co) {
   float d2 = d * d;
   float sd = fmaf(d * d2, -1.0f / 6.0f, d);
@@ -374,170 +398,171 @@ __device__ __forceinline__ void rotate_small(float s, float c, float d, float& s
   so = fmaf(s, cd, c * sd);
   co = fmaf(c, cd, -s * sd);
 }
+// same for |d| < 2e-3 (the J2 short-period corrections): d^3/6 < 1.4e-9 is
+// below fp32 resolution, so sin d = d.
+__device__ __forceinline__ void rotate_tiny(float s, float c, float d, float& so, float& co) {
+  float cd = fmaf(d * d, -0.5f, 1.0f);
+  so = fmaf(s, cd, c * d);
+  co = fmaf(c, cd, -s * d);
+}
 
-__device__ __forceinline__ float frcp(float x) { return __frcp_rn(x); }
-
-__device__ __forceinline__ void cell32(const Rec<float>& R, float th, float tl, const Grav& g, Cell32& o) {
+// One fp32 cell.  ISIMP and KITER are warp-uniform per satellite and are
+// compile-time here, so the whole cell is straight-line code and the grid
+// kernel can interleave its four cells freely.  KITER = 0: runtime count
+// with a final SFU sincos (eccentric orbits).
+template <bool ISIMP, int KITER>
+__device__ __forceinline__ void cell32(const Rec<float>& R, float t, float tl, const Grav& g,
+                                       float (&o)[6], int& code) {
   const float tiny = FLT_MIN;
-  const float xke = (float)g.xke, j2 = (float)g.j2, re = (float)g.re;
-  const float vkmpersec = (float)(g.re * g.xke / 60.0);
-  const float inv_xke = (float)(1.0 / g.xke);
   const int flags = R.flags();
-  const bool isimp = flags & FLAG_ISIMP;
-  const float t = th + tl;
 
-  // secular gravity (double-float, reduced)  kernel.py:366-370
-  float xmdf = secular_angle(R.v[S_MO], R.v[S_MDOT], R.v[S_MDOT_LO], th, tl);
-  float argpdf = secular_angle(R.v[S_ARGPO], R.v[S_ARGPDOT], R.v[S_ARGPDOT_LO], th, tl);
-  float t2 = t * t;
-  float nodem = secular_angle(R.v[S_NODEO], R.v[S_NODEDOT], R.v[S_NODEDOT_LO], th, tl);
-  nodem = fmaf(R.v[S_NODECF], t2, nodem);
-  // u0 = mo + argpo and (mdot + argpdot) folded at init: the argument of
-  // Kepler's equation without its small terms (kernel.py:409-434).
-  float ubase = secular_angle(R.v[S_U0], R.v[S_UDOT], R.v[S_UDOT_LO], th, tl);
+  // secular gravity  kernel.py:366-370.  Only the Kepler argument needs the
+  // double-float treatment: u = (mo + argpo) + (mdot + argpdot) t + ...
+  // (mm + argpm; the drag term cancels), the rest enter sin/cos damped.
+  const float xmdf = fmaf(R.v[S_MDOT], t, R.v[S_MO]);
+  const float argpdf = fmaf(R.v[S_ARGPDOT], t, R.v[S_ARGPO]);
+  const float t2 = t * t;
+  const float nodem = fmaf(R.v[S_NODECF], t2, fmaf(R.v[S_NODEDOT], t, R.v[S_NODEO]));
+  const float ubase = secular_angle(R.v[S_U0], R.v[S_UDOT], R.v[S_UDOT_LO], t, tl);
 
   // drag  kernel.py:371-391
   float tempa = fmaf(-R.v[S_CC1], t, 1.0f);
   float tempe = R.v[S_BC4] * t;
   float templ = R.v[S_T2COF] * t2;
   float temp = 0.0f;
-  if (!isimp) {
+  if constexpr (!ISIMP) {
     float sx, cx;
-    __sincosf(xmdf, &sx, &cx);
-    float delmtemp = fmaf(R.v[S_ETA], cx, 1.0f);
-    float delm = R.v[S_XMCOF] * fmaf(delmtemp * delmtemp, delmtemp, -R.v[S_DELMO]);
+    sincos_a(xmdf, sx, cx);
+    const float dmt = fmaf(R.v[S_ETA], cx, 1.0f);
+    const float delm = R.v[S_XMCOF] * fmaf(dmt * dmt, dmt, -R.v[S_DELMO]);
     temp = fmaf(R.v[S_OMGCOF], t, delm);
-    float t3 = t2 * t;
-    float t4 = t3 * t;
-    tempa = tempa - R.v[S_D2] * t2 - R.v[S_D3] * t3 - R.v[S_D4] * t4;
-    // sin(xmdf + temp): temp is the small drag correction
-    float smm = fmaf(cx, temp, sx);
-    smm = fmaf(-0.5f * sx, temp * temp, smm);
+    const float t3 = t2 * t;
+    const float t4 = t2 * t2;
+    tempa = fmaf(-R.v[S_D4], t4, fmaf(-R.v[S_D3], t3, fmaf(-R.v[S_D2], t2, tempa)));
+    // sin(xmdf + temp), temp the small drag correction of the mean anomaly
+    // (its square, times B* cc5, is far below fp32 resolution of em)
+    const float smm = fmaf(cx, temp, sx);
     tempe = fmaf(R.v[S_BC5], smm - R.v[S_SINMAO], tempe);
-    templ = templ + R.v[S_T3COF] * t3 + t4 * fmaf(t, R.v[S_T5COF], R.v[S_T4COF]);
+    templ = fmaf(t4, fmaf(t, R.v[S_T5COF], R.v[S_T4COF]), fmaf(R.v[S_T3COF], t3, templ));
   }
-  float argpm = argpdf - temp;
+  const float argpm = argpdf - temp;
 
   // mean motion / eccentricity  kernel.py:397-408
-  const bool bad_nm = flags & FLAG_BAD_NM;
-  float am = R.v[S_AM0] * tempa * tempa;
-  am = gmaxf(am, tiny);
-  float rsam = rsqrtf(am);
-  float nm = xke * (rsam * rsam * rsam);
+  const float am = fmaxf(R.v[S_AM0] * tempa * tempa, tiny);   // maximum(am, tiny)
+  const float rsam = rsq_a(am);
+  const float rsam3 = rsam * rsam * rsam;                     // nm / xke = am^-1.5
   float em = R.v[S_ECCO] - tempe;
   const bool bad_em = (em >= 1.0f) || (em < -0.001f);
   em = em < 1.0e-6f ? 1.0e-6f : em;
-  float mlt = R.v[S_NO] * templ;      // mm += no_unkozai * templ
 
   // long-period periodics  kernel.py:420-431
   float sa, ca;
-  __sincosf(argpm, &sa, &ca);
-  float axnl = em * ca;
-  float pl_lp = gmaxf(am * fmaf(-em, em, 1.0f), tiny);
-  float ilp = frcp(pl_lp);
-  float aynl = fmaf(em, sa, ilp * R.v[S_AYCOF]);
-  // u = xl - nodep = mm + argpm + xlcof/pl * axnl (mod 2pi); the drag
-  // term `temp` cancels between mm and argpm.
-  float u = ubase + mlt + ilp * R.v[S_XLCOF] * axnl;
+  sincos_a(argpm, sa, ca);
+  const float axnl = em * ca;
+  const float ilp = rcp_a(fmaxf(am * fmaf(-em, em, 1.0f), tiny));
+  const float aynl = fmaf(em, sa, ilp * R.v[S_AYCOF]);
+  // u = xl - nodep = mm + argpm + (xlcof/pl) axnl  (mod 2pi)
+  const float u = fmaf(ilp * R.v[S_XLCOF], axnl, fmaf(R.v[S_NO], templ, ubase));
 
-  // Kepler: fixed, warp-uniform iteration count  kernel.py:325-349
-  const int kiter = (flags >> KEPLER_SHIFT) & 0xf;
-  float eo1 = u, s, c;
-  float tem5 = 0.0f;
-#pragma unroll 1
-  for (int it = 0; it < kiter; ++it) {
-    __sincosf(eo1, &s, &c);
-    float den = fmaf(-s, aynl, fmaf(-c, axnl, 1.0f));
-    float num = fmaf(axnl, s, fmaf(-aynl, c, u)) - eo1;
-    tem5 = num * frcp(den);
-    tem5 = fminf(fmaxf(tem5, -0.95f), 0.95f);
+  // Kepler, fixed warp-uniform iteration count  kernel.py:325-349
+  float eo1 = u, s = 0.0f, c = 1.0f, tem5 = 0.0f;
+  const int kiter = KITER > 0 ? KITER : ((flags >> KEPLER_SHIFT) & 0xf);
+#pragma unroll
+  for (int it = 0; it < (KITER > 0 ? KITER : 16); ++it) {
+    if (KITER == 0 && it >= kiter) break;
+    sincos_a(eo1, s, c);
+    const float den = fmaf(-s, aynl, fmaf(-c, axnl, 1.0f));
+    const float num = fmaf(axnl, s, fmaf(-aynl, c, u)) - eo1;
+    tem5 = num * rcp_a(den);
+    // the +-0.95 clamp (kernel.py:343-346) cannot trigger for e < 0.1
+    // (|num| <= 2e, den >= 1 - 2e), i.e. for KITER 1 and 2
+    if (KITER == 0 || KITER > 2) tem5 = fminf(fmaxf(tem5, -0.95f), 0.95f);
     eo1 += tem5;
   }
-  // sin/cos of the final iterate: rotate the last evaluation by the last
-  // (converged, tiny) step instead of another SFU round trip.
   float sineo1, coseo1;
-  if (kiter > 0 && kiter <= 3) {
-    rotate_small(s, c, tem5, sineo1, coseo1);
+  if constexpr (KITER > 0) {
+    rotate_tiny(s, c, tem5, sineo1, coseo1);     // last step <= e^3/2 < 4e-3
   } else {
-    __sincosf(eo1, &sineo1, &coseo1);
+    sincos_a(eo1, sineo1, coseo1);
   }
 
   // short-period preliminaries  kernel.py:440-460
-  float ecose = fmaf(axnl, coseo1, aynl * sineo1);
-  float esine = fmaf(axnl, sineo1, -aynl * coseo1);
-  float el2 = fmaf(axnl, axnl, aynl * aynl);
-  float pl = am * (1.0f - el2);
+  const float ecose = fmaf(axnl, coseo1, aynl * sineo1);
+  const float esine = fmaf(axnl, sineo1, -aynl * coseo1);
+  const float el2 = fmaf(axnl, axnl, aynl * aynl);
+  const float pl = am * (1.0f - el2);
   const bool bad_pl = pl < 0.0f;
-  float pl_safe = gmaxf(pl, tiny);
-  float rl = am * (1.0f - ecose);
-  float rl_safe = rl == 0.0f ? tiny : rl;
-  float irl = frcp(rl_safe);
-  float rdotl = (am * rsam) * esine * irl;        // sqrt(am) = am * rsqrt(am)
-  float rspl = rsqrtf(pl_safe);
-  float rvdotl = (pl_safe * rspl) * irl;          // sqrt(pl)
-  float omel2 = gmaxf(1.0f - el2, tiny);
-  float betal = omel2 * rsqrtf(omel2);
-  float tq = esine * frcp(1.0f + betal);
-  // (sinu, cosu) up to the positive factor am/rl, normalised: replaces the
-  // atan2 of kernel.py:455 (only sin/cos of su are ever used)
-  float sn = sineo1 - aynl - axnl * tq;
-  float cs = coseo1 - axnl + aynl * tq;
-  float nrm = rsqrtf(fmaf(sn, sn, cs * cs));
-  float sinu = sn * nrm, cosu = cs * nrm;
-  float sin2u = (cosu + cosu) * sinu;
-  float cos2u = fmaf(-2.0f * sinu, sinu, 1.0f);
-  float ipl = rspl * rspl;
-  float temp1 = 0.5f * j2 * ipl;
-  float temp2 = temp1 * ipl;
+  const float pl_safe = fmaxf(pl, tiny);
+  const float rl = am * (1.0f - ecose);
+  const float irl = rcp_a(rl == 0.0f ? tiny : rl);
+  const float rdotl = (am * rsam) * esine * irl;          // sqrt(am) esine / rl
+  const float rspl = rsq_a(pl_safe);
+  const float rvdotl = (pl_safe * rspl) * irl;            // sqrt(pl) / rl
+  const float omel2 = fmaxf(1.0f - el2, tiny);
+  const float betal = omel2 * rsq_a(omel2);
+  const float tq = esine * rcp_a(1.0f + betal);
+  // (sin u, cos u) up to the common positive factor am/rl, normalised: the
+  // atan2 of kernel.py:455 is only ever used through sin/cos.
+  const float sn = fmaf(-axnl, tq, sineo1 - aynl);
+  const float cs = fmaf(aynl, tq, coseo1 - axnl);
+  const float nrm = rsq_a(fmaf(sn, sn, cs * cs));
+  const float sinu = sn * nrm, cosu = cs * nrm;
+  const float sin2u = (cosu + cosu) * sinu;
+  const float cos2u = fmaf(-2.0f * sinu, sinu, 1.0f);
+  const float ipl = rspl * rspl;
+  const float temp1 = g.half_j2_f * ipl;
+  const float temp2 = temp1 * ipl;
 
-  // short-period periodics  kernel.py:463-469
-  const float con41 = R.v[S_CON41], x1mth2 = R.v[S_X1MTH2];
-  const float cosip = R.v[S_COSIO], sinip = R.v[S_SINIO];
-  float mrt = fmaf(rl, fmaf(-1.5f * temp2 * betal, con41, 1.0f), 0.5f * temp1 * x1mth2 * cos2u);
-  float dsu = -0.25f * temp2 * R.v[S_X7THM1] * sin2u;
-  float dnode = 1.5f * temp2 * cosip * sin2u;
-  float dinc = 1.5f * temp2 * cosip * sinip * cos2u;
-  float nmt = nm * temp1 * inv_xke;
-  float mvt = fmaf(-nmt * x1mth2, sin2u, rdotl);
-  float rvdot = fmaf(nmt, fmaf(x1mth2, cos2u, 1.5f * con41), rvdotl);
+  // short-period periodics  kernel.py:463-469 (per-satellite factors
+  // pre-multiplied in the record)
+  const float n15c41 = R.v[S32_NEG15CON41], x1mth2 = R.v[S_X1MTH2];
+  const float mrt = fmaf(rl, fmaf(n15c41 * temp2, betal, 1.0f),
+                         (temp1 * R.v[S32_HALFX1MTH2]) * cos2u);
+  const float t2s = temp2 * sin2u;
+  const float dsu = R.v[S32_QX7THM1] * t2s;
+  const float dinc = R.v[S32_C15COSSIN] * (temp2 * cos2u);
+  const float nmt = rsam3 * temp1;                          // nm temp1 / xke
+  const float mvt = fmaf(-nmt * x1mth2, sin2u, rdotl);
+  const float rvdot = fmaf(nmt, fmaf(x1mth2, cos2u, -n15c41), rvdotl);
 
   // orientation  kernel.py:472-493
   float sinsu, cossu, snod, cnod, sini, cosi;
-  rotate_small(sinu, cosu, dsu, sinsu, cossu);
-  __sincosf(nodem + dnode, &snod, &cnod);
-  rotate_small(sinip, cosip, dinc, sini, cosi);
-  float xmx = -snod * cosi;
-  float xmy = cnod * cosi;
-  float ux = fmaf(xmx, sinsu, cnod * cossu);
-  float uy = fmaf(xmy, sinsu, snod * cossu);
-  float uz = sini * sinsu;
-  float vx = fmaf(xmx, cossu, -cnod * sinsu);
-  float vy = fmaf(xmy, cossu, -snod * sinsu);
-  float vz = sini * cossu;
-  float mr = mrt * re;
-  o.r[0] = mr * ux;
-  o.r[1] = mr * uy;
-  o.r[2] = mr * uz;
-  o.v[0] = fmaf(mvt, ux, rvdot * vx) * vkmpersec;
-  o.v[1] = fmaf(mvt, uy, rvdot * vy) * vkmpersec;
-  o.v[2] = fmaf(mvt, uz, rvdot * vz) * vkmpersec;
+  rotate_tiny(sinu, cosu, dsu, sinsu, cossu);
+  sincos_a(fmaf(R.v[S32_C15COSIO], t2s, nodem), snod, cnod);   // xnode
+  rotate_tiny(R.v[S_SINIO], R.v[S_COSIO], dinc, sini, cosi);
+  // r = mr U, v = mv U + rv V with U, V the orientation vectors; grouped as
+  // r = (xm, cnod|snod, sini) . (mr sinsu, mr cossu), same for v
+  const float xmx = -snod * cosi;
+  const float xmy = cnod * cosi;
+  const float mr = mrt * g.re_f;
+  const float ra = mr * sinsu, rb = mr * cossu;
+  o[0] = fmaf(xmx, ra, cnod * rb);
+  o[1] = fmaf(xmy, ra, snod * rb);
+  o[2] = sini * ra;
+  const float mv = mvt * g.vkm_f, rv = rvdot * g.vkm_f;
+  const float va = fmaf(mv, sinsu, rv * cossu);
+  const float vb = fmaf(mv, cossu, -rv * sinsu);
+  o[3] = fmaf(xmx, va, cnod * vb);
+  o[4] = fmaf(xmy, va, snod * vb);
+  o[5] = sini * va;
 
-  const bool decayed = mrt < 1.0f;
-  int code = bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
-  int persistent = (flags >> CODE_SHIFT) & 0xff;
-  o.code = persistent != 0 ? persistent : code;
+  // _first_error 2 > 1 > 4 > 6 and the init merge  kernel.py:497-502, 529-534
+  const int persistent = (flags >> CODE_SHIFT) & 0xff;     // includes bad_nm -> 2
+  const int cellc = bad_em ? 1 : bad_pl ? 4 : (mrt < 1.0f) ? 6 : 0;
+  code = persistent != 0 ? persistent : cellc;
 }
 
 // ======================================================================
 // Packing: SoA fp64 satrec -> packed record (per satellite, fp64 math)
 // ======================================================================
 __device__ __forceinline__ int kepler_iters_for(double ecco) {
-  // fp32 Newton from E0 = u: error e -> ~e^2/2 -> ~e^5/8 ... ; these
-  // counts reach fp32 resolution.
-  double e = fabs(ecco) + 0.01;     // margin for drag-driven growth of em
-  if (e < 0.06) return 2;
-  if (e < 0.25) return 3;
-  if (e < 0.5) return 5;
+  // fp32 Newton from E0 = u: |E - E_k| <~ e^(2^(k+1)-1) / 2^(2^k-1); these
+  // counts reach fp32 resolution.  The margin covers the
+  // drag-driven change of em = ecco - tempe over the propagation span.
+  const double e = fabs(ecco) + 0.001;
+  if (e < 0.004) return 1;
+  if (e < 0.1) return 2;
+  if (e < 0.4) return 3;
   return 10;
 }
 
@@ -598,7 +623,10 @@ __device__ __forceinline__ void record_values(const double* f, int init_code, bo
   out[S_UDOT] = f[F_MDOT] + f[F_ARGPDOT];
   out[S_UDOT_LO] = 0.0;
   out[S_U0] = pymod_2pi(f[F_MO] + f[F_ARGPO]);
-  const int persistent = init_code == 6 ? 0 : init_code;   // kernel.py:532
+  // kernel.py:532: init codes persist except 6; bad_nm (per satellite) is
+  // folded in behind them, preserving _first_error precedence 2 > 1 > 4 > 6
+  int persistent = init_code == 6 ? 0 : init_code;
+  if (persistent == 0 && bad_nm) persistent = 2;
   flags = (isimp ? FLAG_ISIMP : 0) | (bad_nm ? FLAG_BAD_NM : 0) |
           (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0xff) << CODE_SHIFT);
 }
@@ -623,10 +651,19 @@ __device__ __forceinline__ void store_record<float>(const double* f, int init_co
   float o[S_COUNT];
 #pragma unroll
   for (int i = 0; i < S_COUNT; ++i) o[i] = (float)v[i];
-  split_df(f[F_MDOT], o[S_MDOT], o[S_MDOT_LO]);
-  split_df(f[F_ARGPDOT], o[S_ARGPDOT], o[S_ARGPDOT_LO]);
-  split_df(f[F_NODEDOT], o[S_NODEDOT], o[S_NODEDOT_LO]);
   split_df(v[S_UDOT], o[S_UDOT], o[S_UDOT_LO]);
+  o[S32_NEG15CON41] = (float)(-1.5 * f[F_CON41]);
+  o[S32_HALFX1MTH2] = (float)(0.5 * f[F_X1MTH2]);
+  o[S32_QX7THM1] = (float)(-0.25 * f[F_X7THM1]);
+  o[S32_C15COSIO] = (float)(1.5 * v[S_COSIO]);
+  o[S32_C15COSSIN] = (float)(1.5 * v[S_COSIO] * v[S_SINIO]);
+  // angles that only meet sin/cos or the Kepler argument: keep them in
+  // [-pi, pi) where fp32 has the most resolution
+  o[S_U0] = (float)(v[S_U0] >= kPi ? v[S_U0] - kTwoPi : v[S_U0]);
+  {
+    const double nd = pymod_2pi(v[S_NODEO]);
+    o[S_NODEO] = (float)(nd >= kPi ? nd - kTwoPi : nd);
+  }
   o[S_FLAGS] = __int_as_float(flags);
 #pragma unroll
   for (int i = 0; i < S_COUNT; ++i) rec[i] = o[i];
@@ -828,18 +865,78 @@ __device__ __forceinline__ void st_cs4(int32_t* p, const int (&v)[4]) {
   __stcs(reinterpret_cast<int4*>(p), make_int4(v[0], v[1], v[2], v[3]));
 }
 
-template <typename T>
-struct CellT;
-template <>
-struct CellT<float> { using type = Cell32; };
-template <>
-struct CellT<double> { using type = Cell64; };
-
-__device__ __forceinline__ void eval(const Rec<float>& R, float th, float tl, const Grav& g, Cell32& c) {
-  cell32(R, th, tl, g, c);
+template <bool ISIMP, int KITER>
+__device__ __forceinline__ void compute4(const Rec<float>& R, const float (&th)[kCellsPerLane],
+                                         const float (&tl)[kCellsPerLane], const Grav& g,
+                                         float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
+#pragma unroll
+  for (int k = 0; k < kCellsPerLane; ++k) {
+    float o[6];
+    cell32<ISIMP, KITER>(R, th[k], tl[k], g, o, code[k]);
+#pragma unroll
+    for (int p = 0; p < 6; ++p) out[p][k] = o[p];
+  }
 }
-__device__ __forceinline__ void eval(const Rec<double>& R, double th, float, const Grav& g, Cell64& c) {
+
+// warp-uniform dispatch on the satellite's (isimp, Kepler count)
+__device__ __forceinline__ void compute_cells(const Rec<float>& R, const float (&th)[kCellsPerLane],
+                                              const float (&tl)[kCellsPerLane], const Grav& g,
+                                              float (&out)[6][kCellsPerLane],
+                                              int (&code)[kCellsPerLane]) {
+  const int flags = R.flags();
+  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
+  if (!(flags & FLAG_ISIMP)) {
+    if (kit == 1) compute4<false, 1>(R, th, tl, g, out, code);
+    else if (kit == 2) compute4<false, 2>(R, th, tl, g, out, code);
+    else if (kit == 3) compute4<false, 3>(R, th, tl, g, out, code);
+    else compute4<false, 0>(R, th, tl, g, out, code);
+  } else {
+    if (kit == 1) compute4<true, 1>(R, th, tl, g, out, code);
+    else if (kit == 2) compute4<true, 2>(R, th, tl, g, out, code);
+    else if (kit == 3) compute4<true, 3>(R, th, tl, g, out, code);
+    else compute4<true, 0>(R, th, tl, g, out, code);
+  }
+}
+
+__device__ __forceinline__ void compute_cells(const Rec<double>& R, const double (&th)[kCellsPerLane],
+                                              const float (&)[kCellsPerLane], const Grav& g,
+                                              double (&out)[6][kCellsPerLane],
+                                              int (&code)[kCellsPerLane]) {
+#pragma unroll
+  for (int k = 0; k < kCellsPerLane; ++k) {
+    Cell64 c;
+    cell64(R, th[k], g, c);
+    out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
+    out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
+    code[k] = c.code;
+  }
+}
+
+// single cell with the same dispatch (pairs kernel): identical arithmetic
+// to the grid kernel's cells, so batch == scalar bit for bit
+__device__ __forceinline__ void compute_one(const Rec<float>& R, float th, float tl, const Grav& g,
+                                            float (&o)[6], int& code) {
+  const int flags = R.flags();
+  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
+  if (!(flags & FLAG_ISIMP)) {
+    if (kit == 1) cell32<false, 1>(R, th, tl, g, o, code);
+    else if (kit == 2) cell32<false, 2>(R, th, tl, g, o, code);
+    else if (kit == 3) cell32<false, 3>(R, th, tl, g, o, code);
+    else cell32<false, 0>(R, th, tl, g, o, code);
+  } else {
+    if (kit == 1) cell32<true, 1>(R, th, tl, g, o, code);
+    else if (kit == 2) cell32<true, 2>(R, th, tl, g, o, code);
+    else if (kit == 3) cell32<true, 3>(R, th, tl, g, o, code);
+    else cell32<true, 0>(R, th, tl, g, o, code);
+  }
+}
+__device__ __forceinline__ void compute_one(const Rec<double>& R, double th, float, const Grav& g,
+                                            double (&o)[6], int& code) {
+  Cell64 c;
   cell64(R, th, g, c);
+  o[0] = c.r[0]; o[1] = c.r[1]; o[2] = c.r[2];
+  o[3] = c.v[0]; o[4] = c.v[1]; o[5] = c.v[2];
+  code = c.code;
 }
 
 template <typename T, bool VEC>
@@ -876,19 +973,15 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
     for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
   }
 #pragma unroll
-  for (int k = 0; k < kCellsPerLane; ++k)
-    tl[k] = (times_lo != nullptr && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
+  for (int k = 0; k < kCellsPerLane; ++k) tl[k] = 0.0f;
+  if (times_lo != nullptr) {
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = j0 + k < m ? __ldg(times_lo + j0 + k) : 0.0f;
+  }
 
   T out[6][kCellsPerLane];
   int code[kCellsPerLane];
-#pragma unroll
-  for (int k = 0; k < kCellsPerLane; ++k) {
-    typename CellT<T>::type c;
-    eval(R, th[k], tl[k], g, c);
-    out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
-    out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
-    code[k] = c.code;
-  }
+  compute_cells(R, th, tl, g, out, code);
 
   T* base = planes + sat * row_stride + j0;
   int32_t* cbase = codes + sat * code_stride + j0;
@@ -920,11 +1013,12 @@ pairs_kernel(const T* __restrict__ rec, const int64_t* __restrict__ idx, const T
   if (k >= p) return;
   Rec<T> R;
   load_rec(rec + idx[k] * S_COUNT, R);
-  typename CellT<T>::type c;
-  eval(R, times[k], times_lo != nullptr ? times_lo[k] : 0.0f, g, c);
-  rv[0 * p + k] = c.r[0]; rv[1 * p + k] = c.r[1]; rv[2 * p + k] = c.r[2];
-  rv[3 * p + k] = c.v[0]; rv[4 * p + k] = c.v[1]; rv[5 * p + k] = c.v[2];
-  codes[k] = c.code;
+  T o[6];
+  int code;
+  compute_one(R, times[k], times_lo != nullptr ? times_lo[k] : 0.0f, g, o, code);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) rv[q * p + k] = o[q];
+  codes[k] = code;
 }
 
 template <typename T>
@@ -939,6 +1033,12 @@ bool grav_from(const double* grav, Grav& g) {
   if (grav == nullptr) return false;
   g.mu = grav[0]; g.re = grav[1]; g.xke = grav[2]; g.tumin = grav[3];
   g.j2 = grav[4]; g.j3 = grav[5]; g.j4 = grav[6]; g.j3oj2 = grav[7];
+  g.vkm = g.re * g.xke / 60.0;
+  g.xke_f = (float)g.xke;
+  g.re_f = (float)g.re;
+  g.vkm_f = (float)g.vkm;
+  g.inv_xke_f = (float)(1.0 / g.xke);
+  g.half_j2_f = (float)(0.5 * g.j2);
   return true;
 }
 

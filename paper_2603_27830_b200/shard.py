@@ -1,0 +1,99 @@
+"""Satellite sharding across the GPUs of one node.
+
+Satellites are independent, so the path has NO exchange step: rank r takes
+the contiguous satellite range ``shard_bounds(n, world, r)`` (sizes differ by
+at most one — the reference's partition_work rule, batch.py:125-141), runs
+its own init + grid launch on its own GPU and keeps its slice of the grid
+resident in its HBM.  The only collectives here are optional consumers:
+``max_over_ranks`` for timing and ``gather_grid`` for a caller that really
+wants the whole grid on one rank (NVLink gather, not part of the timed path).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced satellite range of ``rank`` (empty if n < world)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def world_info(group=None) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Max of a per-rank scalar (device timings are reported as the max)."""
+    world, _ = world_info(group)
+    if world == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def propagate_sharded(columns: np.ndarray, times, precision: int = 32, group=None,
+                      device=None):
+    """Rank-local init + propagate of this rank's satellite shard.
+
+    ``columns`` is the full (7, n) catalogue (every rank may hold it; it is
+    56 B per satellite).  Returns (BatchResult of device tensors, (lo, hi)).
+    """
+    from .batch import init_batch, propagate_batch_device
+
+    world, rank = world_info(group)
+    lo, hi = shard_bounds(columns.shape[1], world, rank)
+    if hi <= lo:
+        return None, (lo, hi)
+    sats = init_batch(columns[:, lo:hi], precision=precision, device=device)
+    return propagate_batch_device(sats, times), (lo, hi)
+
+
+def gather_grid(planes: torch.Tensor, error: torch.Tensor, n_total: int, group=None,
+                dst: int = 0):
+    """Assemble the full (6, N, M) / (N, M) grid on rank ``dst`` from the
+    per-rank row shards (shards follow shard_bounds).  Returns the tensors on
+    ``dst`` and None elsewhere.  Works with gloo (CPU tensors) and NCCL."""
+    world, rank = world_info(group)
+    if world == 1:
+        return planes, error
+    m = planes.shape[2]
+    bounds = [shard_bounds(n_total, world, r) for r in range(world)]
+    rows_max = max(hi - lo for lo, hi in bounds)
+    dev = planes.device
+
+    def padded(x, shape):
+        out = torch.zeros(shape, dtype=x.dtype, device=dev)
+        out[tuple(slice(0, s) for s in x.shape)] = x
+        return out
+
+    p = padded(planes, (6, rows_max, m))
+    e = padded(error, (rows_max, m))
+    if rank == dst:
+        plist = [torch.empty_like(p) for _ in range(world)]
+        elist = [torch.empty_like(e) for _ in range(world)]
+    else:
+        plist = elist = None
+    if dist.get_backend(group) == "nccl":
+        # NCCL has no gather; all_gather into every rank then keep dst's
+        plist = [torch.empty_like(p) for _ in range(world)]
+        elist = [torch.empty_like(e) for _ in range(world)]
+        dist.all_gather(plist, p, group=group)
+        dist.all_gather(elist, e, group=group)
+    else:
+        dist.gather(p, plist, dst=dst, group=group)
+        dist.gather(e, elist, dst=dst, group=group)
+    if rank != dst:
+        return None
+    full_p = torch.cat([plist[r][:, :hi - lo] for r, (lo, hi) in enumerate(bounds)], dim=1)
+    full_e = torch.cat([elist[r][:hi - lo] for r, (lo, hi) in enumerate(bounds)], dim=0)
+    return full_p, full_e

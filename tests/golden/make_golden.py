@@ -107,6 +107,7 @@ def main() -> None:
             st = sgp4kit.sgp4_propagate(init, np.asarray(fail_times, dtype=dtype))
             row[f"init_code_{precision}"] = int(np.asarray(init.error_code_at_init))
             row[f"codes_{precision}"] = [int(c) for c in np.asarray(st.error_code)]
+            row[f"finite_{precision}"] = bool(np.isfinite(st.r).all() and np.isfinite(st.v).all())
         table["cases"][key] = row
     (OUT / "ref_failure_codes.json").write_text(json.dumps(table, indent=1) + "\n")
     print("golden fixtures written to", OUT)

@@ -101,7 +101,8 @@ def test_failure_modes(failure_table, precision):
     for k, (key, row) in enumerate(failure_table["cases"].items()):
         assert int(sats.error_codes[k]) == row[f"init_code_{precision}"], key
         assert res.error[k].tolist() == row[f"codes_{precision}"], key
-        assert np.isfinite(res.planes[:, k]).all(), key
+        if row[f"finite_{precision}"]:       # the reference itself overflows on 2 cases
+            assert np.isfinite(res.planes[:, k]).all(), key
 
 
 def test_init_constants_vs_oracle(oracle, golden_columns, golden_states):
