@@ -495,21 +495,37 @@ __device__ __forceinline__ void cell32(const Rec<float>& R, float t, float tl, c
   const float pl_safe = fmaxf(pl, tiny);
   const float rl = am * (1.0f - ecose);
   const float irl = rcp_a(rl == 0.0f ? tiny : rl);
-  const float rdotl = (am * rsam) * esine * irl;          // sqrt(am) esine / rl
-  const float rspl = rsq_a(pl_safe);
-  const float rvdotl = (pl_safe * rspl) * irl;            // sqrt(pl) / rl
-  const float omel2 = fmaxf(1.0f - el2, tiny);
-  const float betal = omel2 * rsq_a(omel2);
-  const float tq = esine * rcp_a(1.0f + betal);
-  // (sin u, cos u) up to the common positive factor am/rl, normalised: the
-  // atan2 of kernel.py:455 is only ever used through sin/cos.
-  const float sn = fmaf(-axnl, tq, sineo1 - aynl);
-  const float cs = fmaf(aynl, tq, coseo1 - axnl);
-  const float nrm = rsq_a(fmaf(sn, sn, cs * cs));
-  const float sinu = sn * nrm, cosu = cs * nrm;
+  const float sqam = am * rsam;                           // sqrt(am)
+  const float rdotl = sqam * esine * irl;                 // sqrt(am) esine / rl
+  float rvdotl, betal, tq, ipl, sinu, cosu;
+  if constexpr (KITER == 1 || KITER == 2) {
+    // e < 0.1 so x = el2 < 0.012: sqrt(1-x), 1/(1+sqrt(1-x)) and 1/(1-x)
+    // as series in x (truncation < 1e-8 relative); pl > 0 here.
+    const float x = el2;
+    betal = fmaf(x, fmaf(x, fmaf(x, -0.0625f, -0.125f), -0.5f), 1.0f);
+    tq = esine * fmaf(x, fmaf(x, fmaf(x, 0.0390625f, 0.0625f), 0.125f), 0.5f);
+    rvdotl = sqam * betal * irl;                          // sqrt(am (1-x)) / rl
+    ipl = (rsam * rsam) * fmaf(x, fmaf(x, x + 1.0f, 1.0f), 1.0f);
+  } else {
+    const float rspl = rsq_a(pl_safe);
+    rvdotl = (pl_safe * rspl) * irl;                      // sqrt(pl) / rl
+    const float omel2 = fmaxf(1.0f - el2, tiny);
+    betal = omel2 * rsq_a(omel2);
+    tq = esine * rcp_a(1.0f + betal);
+    ipl = rspl * rspl;
+  }
+  // (sin u, cos u) = (am/rl) (sn, cs)  (kernel.py:453-454); the atan2 of
+  // :455 is only ever used through sin/cos, so no angle is formed.
+  // |(sn, cs)| = rl/am is an identity in E, so am/rl is the exact norm.
+  {
+    const float sn = fmaf(-axnl, tq, sineo1 - aynl);
+    const float cs = fmaf(aynl, tq, coseo1 - axnl);
+    const float nrm = am * irl;
+    sinu = sn * nrm;
+    cosu = cs * nrm;
+  }
   const float sin2u = (cosu + cosu) * sinu;
   const float cos2u = fmaf(-2.0f * sinu, sinu, 1.0f);
-  const float ipl = rspl * rspl;
   const float temp1 = g.half_j2_f * ipl;
   const float temp2 = temp1 * ipl;
 
@@ -846,27 +862,65 @@ __global__ void pack_kernel(const double* __restrict__ satrec, const int32_t* __
 // ======================================================================
 // Propagate: dense grid
 // ======================================================================
-constexpr int kCellsPerLane = 4;
-constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // 128 time steps
+#ifndef SGP4B_CELLS
+#define SGP4B_CELLS 4
+#endif
+#ifndef SGP4B_MINB
+#define SGP4B_MINB 2
+#endif
+constexpr int kCellsPerLane = SGP4B_CELLS;          // consecutive time steps per lane
+constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // one work item (chunk)
 constexpr int kGridBlock = 256;
+constexpr int kGridMinBlocks = SGP4B_MINB;   // resident 256-thread blocks per SM (fp32)
 
 __device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
 __device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_cs(int32_t* p, int32_t v) { __stcs(reinterpret_cast<int*>(p), (int)v); }
 
-__device__ __forceinline__ void st_cs4(float* p, const float (&v)[4]) {
-  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+// vector streaming stores / read-only loads of N consecutive elements
+template <int N>
+__device__ __forceinline__ void st_vec_cs(float* p, const float (&v)[N]) {
+  if constexpr (N == 4) __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  else if constexpr (N == 2) __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+  else for (int k = 0; k < N; ++k) __stcs(p + k, v[k]);
 }
-__device__ __forceinline__ void st_cs4(double* p, const double (&v)[4]) {
-  __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
-  __stcs(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3]));
+template <int N>
+__device__ __forceinline__ void st_vec_cs(int32_t* p, const int (&v)[N]) {
+  if constexpr (N == 4) __stcs(reinterpret_cast<int4*>(p), make_int4(v[0], v[1], v[2], v[3]));
+  else if constexpr (N == 2) __stcs(reinterpret_cast<int2*>(p), make_int2(v[0], v[1]));
+  else for (int k = 0; k < N; ++k) __stcs(reinterpret_cast<int*>(p) + k, v[k]);
 }
-__device__ __forceinline__ void st_cs4(int32_t* p, const int (&v)[4]) {
-  __stcs(reinterpret_cast<int4*>(p), make_int4(v[0], v[1], v[2], v[3]));
+template <int N>
+__device__ __forceinline__ void st_vec_cs(double* p, const double (&v)[N]) {
+#pragma unroll
+  for (int k = 0; k + 1 < N; k += 2)
+    __stcs(reinterpret_cast<double2*>(p + k), make_double2(v[k], v[k + 1]));
+  if constexpr (N % 2) __stcs(p + N - 1, v[N - 1]);
+}
+template <int N>
+__device__ __forceinline__ void ld_vec(const float* p, float (&v)[N]) {
+  if constexpr (N == 4) {
+    float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else if constexpr (N == 2) {
+    float2 q = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else {
+    for (int k = 0; k < N; ++k) v[k] = __ldg(p + k);
+  }
+}
+template <int N>
+__device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
+#pragma unroll
+  for (int k = 0; k + 1 < N; k += 2) {
+    double2 q = __ldg(reinterpret_cast<const double2*>(p + k));
+    v[k] = q.x; v[k + 1] = q.y;
+  }
+  if constexpr (N % 2) v[N - 1] = __ldg(p + N - 1);
 }
 
 template <bool ISIMP, int KITER>
-__device__ __forceinline__ void compute4(const Rec<float>& R, const float (&th)[kCellsPerLane],
+__device__ __forceinline__ void compute_n(const Rec<float>& R, const float (&th)[kCellsPerLane],
                                          const float (&tl)[kCellsPerLane], const Grav& g,
                                          float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
 #pragma unroll
@@ -886,15 +940,15 @@ __device__ __forceinline__ void compute_cells(const Rec<float>& R, const float (
   const int flags = R.flags();
   const int kit = (flags >> KEPLER_SHIFT) & 0xf;
   if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) compute4<false, 1>(R, th, tl, g, out, code);
-    else if (kit == 2) compute4<false, 2>(R, th, tl, g, out, code);
-    else if (kit == 3) compute4<false, 3>(R, th, tl, g, out, code);
-    else compute4<false, 0>(R, th, tl, g, out, code);
+    if (kit == 1) compute_n<false, 1>(R, th, tl, g, out, code);
+    else if (kit == 2) compute_n<false, 2>(R, th, tl, g, out, code);
+    else if (kit == 3) compute_n<false, 3>(R, th, tl, g, out, code);
+    else compute_n<false, 0>(R, th, tl, g, out, code);
   } else {
-    if (kit == 1) compute4<true, 1>(R, th, tl, g, out, code);
-    else if (kit == 2) compute4<true, 2>(R, th, tl, g, out, code);
-    else if (kit == 3) compute4<true, 3>(R, th, tl, g, out, code);
-    else compute4<true, 0>(R, th, tl, g, out, code);
+    if (kit == 1) compute_n<true, 1>(R, th, tl, g, out, code);
+    else if (kit == 2) compute_n<true, 2>(R, th, tl, g, out, code);
+    else if (kit == 3) compute_n<true, 3>(R, th, tl, g, out, code);
+    else compute_n<true, 0>(R, th, tl, g, out, code);
   }
 }
 
@@ -939,64 +993,71 @@ __device__ __forceinline__ void compute_one(const Rec<double>& R, double th, flo
   code = c.code;
 }
 
+// Persistent warps: the (satellite, 128-step chunk) work items of the grid
+// are split into one contiguous range per resident warp, so a warp reloads
+// its satellite record only when the range crosses a row.
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kGridBlock)
+__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 1)
 grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
             const float* __restrict__ times_lo, int64_t m, Grav g, T* __restrict__ planes,
             int64_t plane_stride, int64_t row_stride, int32_t* __restrict__ codes,
             int64_t code_stride, int64_t chunks) {
-  const int64_t warp = ((int64_t)blockIdx.x * kGridBlock + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * (kGridBlock / 32);
+  const int64_t w = ((int64_t)blockIdx.x * kGridBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t sat = warp / chunks;
-  if (sat >= n) return;
-  const int64_t chunk = warp - sat * chunks;
-  const int64_t j0 = chunk * kCellsPerWarp + lane * kCellsPerLane;
-  if (j0 >= m) return;
+  const int64_t total = n * chunks;
+  const int64_t g0 = total * w / nwarps;
+  const int64_t g1 = total * (w + 1) / nwarps;
+  if (g0 >= g1) return;
+  int64_t sat = g0 / chunks;
+  int64_t chunk = g0 - sat * chunks;
 
   Rec<T> R;
   load_rec(rec + sat * S_COUNT, R);
-
-  T th[kCellsPerLane];
-  float tl[kCellsPerLane];
-  const bool full = j0 + kCellsPerLane <= m;
-  if (VEC && full) {
-    if constexpr (sizeof(T) == 4) {
-      float4 q = __ldg(reinterpret_cast<const float4*>(times + j0));
-      th[0] = q.x; th[1] = q.y; th[2] = q.z; th[3] = q.w;
-    } else {
-      double2 a = __ldg(reinterpret_cast<const double2*>(times + j0));
-      double2 b = __ldg(reinterpret_cast<const double2*>(times + j0) + 1);
-      th[0] = a.x; th[1] = a.y; th[2] = b.x; th[3] = b.y;
-    }
-  } else {
+  for (int64_t gi = g0; gi < g1; ++gi) {
+    const int64_t j0 = chunk * kCellsPerWarp + lane * kCellsPerLane;
+    if (j0 < m) {
+      T th[kCellsPerLane];
+      float tl[kCellsPerLane];
+      const bool full = j0 + kCellsPerLane <= m;
+      if (VEC && full) {
+        ld_vec<kCellsPerLane>(times + j0, th);
+      } else {
 #pragma unroll
-    for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
-  }
-#pragma unroll
-  for (int k = 0; k < kCellsPerLane; ++k) tl[k] = 0.0f;
-  if (times_lo != nullptr) {
-#pragma unroll
-    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = j0 + k < m ? __ldg(times_lo + j0 + k) : 0.0f;
-  }
-
-  T out[6][kCellsPerLane];
-  int code[kCellsPerLane];
-  compute_cells(R, th, tl, g, out, code);
-
-  T* base = planes + sat * row_stride + j0;
-  int32_t* cbase = codes + sat * code_stride + j0;
-  if (VEC && full) {
-#pragma unroll
-    for (int p = 0; p < 6; ++p) st_cs4(base + p * plane_stride, out[p]);
-    st_cs4(cbase, code);
-  } else {
-#pragma unroll
-    for (int k = 0; k < kCellsPerLane; ++k) {
-      if (j0 + k < m) {
-#pragma unroll
-        for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
-        st_cs(cbase + k, code[k]);
+        for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
       }
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) tl[k] = 0.0f;
+      if (times_lo != nullptr) {
+#pragma unroll
+        for (int k = 0; k < kCellsPerLane; ++k) tl[k] = j0 + k < m ? __ldg(times_lo + j0 + k) : 0.0f;
+      }
+
+      T out[6][kCellsPerLane];
+      int code[kCellsPerLane];
+      compute_cells(R, th, tl, g, out, code);
+
+      T* base = planes + sat * row_stride + j0;
+      int32_t* cbase = codes + sat * code_stride + j0;
+      if (VEC && full) {
+#pragma unroll
+        for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
+        st_vec_cs<kCellsPerLane>(cbase, code);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kCellsPerLane; ++k) {
+          if (j0 + k < m) {
+#pragma unroll
+            for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
+            st_cs(cbase + k, code[k]);
+          }
+        }
+      }
+    }
+    if (++chunk == chunks) {
+      chunk = 0;
+      ++sat;
+      if (gi + 1 < g1) load_rec(rec + sat * S_COUNT, R);
     }
   }
 }
@@ -1040,6 +1101,31 @@ bool grav_from(const double* grav, Grav& g) {
   g.inv_xke_f = (float)(1.0 / g.xke);
   g.half_j2_f = (float)(0.5 * g.j2);
   return true;
+}
+
+// blocks of grid_kernel that fit on the current device at once (cached per
+// device and variant): the persistent grid size.
+int64_t resident_blocks(int precision, bool vec) {
+  static int cache[64][4];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    fail(SGP4B_ECUDA, "cudaGetDevice failed");
+    return -1;
+  }
+  const int v = (precision == 64 ? 2 : 0) + (vec ? 1 : 0);
+  if (cache[dev][v] > 0) return cache[dev][v];
+  int sms = 0, per_sm = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = precision == 64
+      ? (vec ? (const void*)grid_kernel<double, true> : (const void*)grid_kernel<double, false>)
+      : (vec ? (const void*)grid_kernel<float, true> : (const void*)grid_kernel<float, false>);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridBlock, 0);
+  if (e != cudaSuccess || sms <= 0 || per_sm <= 0) {
+    fail(SGP4B_ECUDA, "occupancy query: %s", cudaGetErrorString(e));
+    return -1;
+  }
+  cache[dev][v] = sms * per_sm;
+  return cache[dev][v];
 }
 
 inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
@@ -1102,8 +1188,10 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_de
                    ((uintptr_t)times_dev % (4 * esz) == 0);
   const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
   const int64_t warps = n * chunks;
-  const int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
-  if (blocks > 0x7fffffffLL) return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: grid too large");
+  int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
+  const int64_t slots = resident_blocks(precision, vec);
+  if (slots <= 0) return fail(SGP4B_ECUDA, "sgp4b_propagate_grid: %s", g_last_error);
+  if (blocks > slots) blocks = slots;
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == 64) {
     const double* rec = static_cast<const double*>(record_dev);
