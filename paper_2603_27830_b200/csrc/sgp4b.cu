@@ -152,8 +152,24 @@ __device__ __forceinline__ double pymod_2pi(double x) {
 template <typename T>
 struct Rec {
   T v[S_COUNT];
+  __device__ __forceinline__ T operator[](int i) const { return v[i]; }
   __device__ __forceinline__ int flags() const;
 };
+
+// a record held in shared memory (one per warp): fields are re-read at use,
+// which lets the register allocator drop them instead of spilling
+template <typename T>
+struct RecS {
+  const T* p;
+  __device__ __forceinline__ T operator[](int i) const { return p[i]; }
+  __device__ __forceinline__ int flags() const;
+};
+template <>
+__device__ __forceinline__ int RecS<float>::flags() const { return __float_as_int(p[S_FLAGS]); }
+template <>
+__device__ __forceinline__ int RecS<double>::flags() const {
+  return (int)__double_as_longlong(p[S_FLAGS]);
+}
 template <>
 __device__ __forceinline__ int Rec<float>::flags() const { return __float_as_int(v[S_FLAGS]); }
 template <>
@@ -350,14 +366,38 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
 }
 
 // ======================================================================
-// fp32 cell: the throughput path
+// fp32 cells: the throughput path, two cells per instruction
 // ======================================================================
-struct Cell32 {
-  float r[3], v[3];
-  int code;
-};
+// Blackwell executes packed dual-fp32 FMUL2/FADD2/FFMA2 (one issue slot, two
+// IEEE results, scalar-broadcast operands allowed).  A lane's consecutive
+// time steps run the identical instruction stream, so cells are evaluated in
+// pairs on V2 = float2; the SFU ops (sin/cos/rcp/rsqrt), compares and
+// selects stay per component.  Every mul/add/fma below is an explicit
+// IEEE-rounded op (no contraction decisions left to the compiler), so a
+// cell's value does not depend on which half of a pair it ran in: the
+// scalar API (pairs kernel) evaluates the same V2 code with both halves
+// equal and matches the grid bit for bit.
 
-// SFU (MUFU) approximations with flush-to-zero: one MUFU each (sin/cos add
+struct V2 {
+  float2 v;
+};
+__device__ __forceinline__ V2 sp(float s) { return {make_float2(s, s)}; }
+__device__ __forceinline__ V2 operator+(V2 a, V2 b) { return {__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ V2 operator-(V2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
+__device__ __forceinline__ V2 operator-(V2 a, V2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ V2 operator*(V2 a, V2 b) { return {__fmul2_rn(a.v, b.v)}; }
+__device__ __forceinline__ V2 fma2(V2 a, V2 b, V2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
+__device__ __forceinline__ V2 operator+(V2 a, float b) { return a + sp(b); }
+__device__ __forceinline__ V2 operator+(float a, V2 b) { return sp(a) + b; }
+__device__ __forceinline__ V2 operator-(float a, V2 b) { return sp(a) - b; }
+__device__ __forceinline__ V2 operator-(V2 a, float b) { return a - sp(b); }
+__device__ __forceinline__ V2 operator*(V2 a, float b) { return a * sp(b); }
+__device__ __forceinline__ V2 operator*(float a, V2 b) { return sp(a) * b; }
+__device__ __forceinline__ V2 fma2(V2 a, V2 b, float c) { return fma2(a, b, sp(c)); }
+__device__ __forceinline__ V2 fma2(V2 a, float b, V2 c) { return fma2(a, sp(b), c); }
+__device__ __forceinline__ V2 fma2(V2 a, float b, float c) { return fma2(a, sp(b), sp(c)); }
+
+// SFU (MUFU) approximations with flush-to-zero, per component (sin/cos add
 // the FMUL by 1/2pi the SFU expects).  Absolute error of sin/cos ~2^-21 on
 // [-pi, pi]; rcp/rsqrt ~1 ulp.
 __device__ __forceinline__ float rcp_a(float x) {
@@ -374,198 +414,204 @@ __device__ __forceinline__ void sincos_a(float x, float& s, float& c) {
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(x));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(x));
 }
+__device__ __forceinline__ V2 rcp2(V2 a) { return {make_float2(rcp_a(a.v.x), rcp_a(a.v.y))}; }
+__device__ __forceinline__ V2 rsq2(V2 a) { return {make_float2(rsq_a(a.v.x), rsq_a(a.v.y))}; }
+__device__ __forceinline__ void sincos2(V2 a, V2& s, V2& c) {
+  sincos_a(a.v.x, s.v.x, c.v.x);
+  sincos_a(a.v.y, s.v.y, c.v.y);
+}
+__device__ __forceinline__ V2 rint2(V2 a) { return {make_float2(rintf(a.v.x), rintf(a.v.y))}; }
+// maximum(x, f) == where(x >= f, x, f): fmaxf has the same NaN behaviour
+__device__ __forceinline__ V2 vmax(V2 a, float f) { return {make_float2(fmaxf(a.v.x, f), fmaxf(a.v.y, f))}; }
+__device__ __forceinline__ V2 clamp95(V2 a) {
+  return {make_float2(fminf(fmaxf(a.v.x, -0.95f), 0.95f), fminf(fmaxf(a.v.y, -0.95f), 0.95f))};
+}
 
 // x0 + (rate_hi + rate_lo) * (t + tl), reduced mod 2*pi, in double-float:
 // p = rate_hi*t rounded, its exact error by fma, k = nearest revolution;
 // p - k*2pi_hi is exact (the difference needs < 24 bits: DESIGN.md §4).
-__device__ __forceinline__ float secular_angle(float x0, float rate, float rate_lo, float t, float tl) {
-  float p = rate * t;
-  float e = fmaf(rate, t, -p);
-  e = fmaf(rate_lo, t, e);
-  e = fmaf(rate, tl, e);
-  float k = rintf(p * kInvTwoPiF);
-  float r = fmaf(-k, kTwoPiHiF, p);
-  r = fmaf(-k, kTwoPiLoF, r);
-  return r + (x0 + e);
+template <bool LO>
+__device__ __forceinline__ V2 secular_angle(float x0, float rate, float rate_lo, V2 t, V2 tl) {
+  const V2 p = t * rate;
+  V2 e = fma2(t, rate, -p);
+  e = fma2(t, rate_lo, e);
+  if constexpr (LO) e = fma2(tl, rate, e);
+  const V2 k = rint2(p * kInvTwoPiF);
+  V2 r = fma2(-k, kTwoPiHiF, p);
+  r = fma2(-k, kTwoPiLoF, r);
+  return r + (e + x0);
 }
 
-// (sin, cos)(a + d) from (sin, cos)(a) for a small angle d (series to
-// d^3 / d^2; |d| < 1e-2 keeps the truncation below fp32 resolution).
-__device__ __forceinline__ void rotate_small(float s, float c, float d, float& so, float& co) {
-  float d2 = d * d;
-  float sd = fmaf(d * d2, -1.0f / 6.0f, d);
-  float cd = fmaf(d2, -0.5f, 1.0f);
-  so = fmaf(s, cd, c * sd);
-  co = fmaf(c, cd, -s * sd);
-}
-// same for |d| < 2e-3 (the J2 short-period corrections): d^3/6 < 1.4e-9 is
-// below fp32 resolution, so sin d = d.
-__device__ __forceinline__ void rotate_tiny(float s, float c, float d, float& so, float& co) {
-  float cd = fmaf(d * d, -0.5f, 1.0f);
-  so = fmaf(s, cd, c * d);
-  co = fmaf(c, cd, -s * d);
+// (sin, cos)(a + d) from (sin, cos)(a) for |d| < 4e-3 (the J2 short-period
+// corrections and the last Newton step): d^3/6 < 1.1e-8 is below fp32
+// resolution, so sin d = d, cos d = 1 - d^2/2.
+__device__ __forceinline__ void rotate_tiny(V2 s, V2 c, V2 d, V2& so, V2& co) {
+  const V2 cd = fma2(d * d, -0.5f, 1.0f);
+  so = fma2(s, cd, c * d);
+  co = fma2(c, cd, (-s) * d);
 }
 
-// One fp32 cell.  ISIMP and KITER are warp-uniform per satellite and are
-// compile-time here, so the whole cell is straight-line code and the grid
-// kernel can interleave its four cells freely.  KITER = 0: runtime count
-// with a final SFU sincos (eccentric orbits).
-template <bool ISIMP, int KITER>
-__device__ __forceinline__ void cell32(const Rec<float>& R, float t, float tl, const Grav& g,
-                                       float (&o)[6], int& code) {
+// Two fp32 cells of one satellite.  ISIMP and KITER are warp-uniform per
+// satellite and compile-time here, so the cell is straight-line code.
+// KITER = 0: runtime Kepler count with a final SFU sincos (eccentric
+// orbits).  `R[i]` is the satellite's packed record (scalar fields).
+template <bool ISIMP, int KITER, bool LO, class RT>
+__device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V2 (&o)[6],
+                                      int (&code)[2]) {
   const float tiny = FLT_MIN;
   const int flags = R.flags();
 
   // secular gravity  kernel.py:366-370.  Only the Kepler argument needs the
   // double-float treatment: u = (mo + argpo) + (mdot + argpdot) t + ...
   // (mm + argpm; the drag term cancels), the rest enter sin/cos damped.
-  const float xmdf = fmaf(R.v[S_MDOT], t, R.v[S_MO]);
-  const float argpdf = fmaf(R.v[S_ARGPDOT], t, R.v[S_ARGPO]);
-  const float t2 = t * t;
-  const float nodem = fmaf(R.v[S_NODECF], t2, fmaf(R.v[S_NODEDOT], t, R.v[S_NODEO]));
-  const float ubase = secular_angle(R.v[S_U0], R.v[S_UDOT], R.v[S_UDOT_LO], t, tl);
+  const V2 xmdf = fma2(t, R[S_MDOT], sp(R[S_MO]));
+  const V2 argpdf = fma2(t, R[S_ARGPDOT], sp(R[S_ARGPO]));
+  const V2 t2 = t * t;
+  const V2 nodem = fma2(t2, R[S_NODECF], fma2(t, R[S_NODEDOT], sp(R[S_NODEO])));
+  const V2 ubase = secular_angle<LO>(R[S_U0], R[S_UDOT], R[S_UDOT_LO], t, tl);
 
   // drag  kernel.py:371-391
-  float tempa = fmaf(-R.v[S_CC1], t, 1.0f);
-  float tempe = R.v[S_BC4] * t;
-  float templ = R.v[S_T2COF] * t2;
-  float temp = 0.0f;
+  V2 tempa = fma2(t, -R[S_CC1], 1.0f);
+  V2 tempe = t * R[S_BC4];
+  V2 templ = t2 * R[S_T2COF];
+  V2 temp = sp(0.0f);
   if constexpr (!ISIMP) {
-    float sx, cx;
-    sincos_a(xmdf, sx, cx);
-    const float dmt = fmaf(R.v[S_ETA], cx, 1.0f);
-    const float delm = R.v[S_XMCOF] * fmaf(dmt * dmt, dmt, -R.v[S_DELMO]);
-    temp = fmaf(R.v[S_OMGCOF], t, delm);
-    const float t3 = t2 * t;
-    const float t4 = t2 * t2;
-    tempa = fmaf(-R.v[S_D4], t4, fmaf(-R.v[S_D3], t3, fmaf(-R.v[S_D2], t2, tempa)));
+    V2 sx, cx;
+    sincos2(xmdf, sx, cx);
+    const V2 dmt = fma2(cx, R[S_ETA], 1.0f);
+    const V2 delm = fma2(dmt * dmt, dmt, sp(-R[S_DELMO])) * R[S_XMCOF];
+    temp = fma2(t, R[S_OMGCOF], delm);
+    const V2 t3 = t2 * t;
+    const V2 t4 = t2 * t2;
+    tempa = fma2(t4, -R[S_D4], fma2(t3, -R[S_D3], fma2(t2, -R[S_D2], tempa)));
     // sin(xmdf + temp), temp the small drag correction of the mean anomaly
     // (its square, times B* cc5, is far below fp32 resolution of em)
-    const float smm = fmaf(cx, temp, sx);
-    tempe = fmaf(R.v[S_BC5], smm - R.v[S_SINMAO], tempe);
-    templ = fmaf(t4, fmaf(t, R.v[S_T5COF], R.v[S_T4COF]), fmaf(R.v[S_T3COF], t3, templ));
+    const V2 smm = fma2(cx, temp, sx);
+    tempe = fma2(smm - R[S_SINMAO], R[S_BC5], tempe);
+    templ = fma2(t4, fma2(t, R[S_T5COF], sp(R[S_T4COF])), fma2(t3, R[S_T3COF], templ));
   }
-  const float argpm = argpdf - temp;
+  const V2 argpm = argpdf - temp;
 
   // mean motion / eccentricity  kernel.py:397-408
-  const float am = fmaxf(R.v[S_AM0] * tempa * tempa, tiny);   // maximum(am, tiny)
-  const float rsam = rsq_a(am);
-  const float rsam3 = rsam * rsam * rsam;                     // nm / xke = am^-1.5
-  float em = R.v[S_ECCO] - tempe;
-  const bool bad_em = (em >= 1.0f) || (em < -0.001f);
-  em = em < 1.0e-6f ? 1.0e-6f : em;
+  const V2 am = vmax(tempa * tempa * R[S_AM0], tiny);        // maximum(am, tiny)
+  const V2 rsam = rsq2(am);
+  const V2 rsam3 = rsam * rsam * rsam;                        // nm / xke = am^-1.5
+  V2 em = R[S_ECCO] - tempe;
+  bool bad_em[2];
+  bad_em[0] = (em.v.x >= 1.0f) || (em.v.x < -0.001f);
+  bad_em[1] = (em.v.y >= 1.0f) || (em.v.y < -0.001f);
+  em.v.x = em.v.x < 1.0e-6f ? 1.0e-6f : em.v.x;
+  em.v.y = em.v.y < 1.0e-6f ? 1.0e-6f : em.v.y;
 
   // long-period periodics  kernel.py:420-431
-  float sa, ca;
-  sincos_a(argpm, sa, ca);
-  const float axnl = em * ca;
-  const float ilp = rcp_a(fmaxf(am * fmaf(-em, em, 1.0f), tiny));
-  const float aynl = fmaf(em, sa, ilp * R.v[S_AYCOF]);
+  V2 sa, ca;
+  sincos2(argpm, sa, ca);
+  const V2 axnl = em * ca;
+  const V2 ilp = rcp2(vmax(am * fma2(-em, em, 1.0f), tiny));
+  const V2 aynl = fma2(em, sa, ilp * R[S_AYCOF]);
   // u = xl - nodep = mm + argpm + (xlcof/pl) axnl  (mod 2pi)
-  const float u = fmaf(ilp * R.v[S_XLCOF], axnl, fmaf(R.v[S_NO], templ, ubase));
+  const V2 u = fma2(ilp * R[S_XLCOF], axnl, fma2(templ, R[S_NO], ubase));
 
   // Kepler, fixed warp-uniform iteration count  kernel.py:325-349
-  float eo1 = u, s = 0.0f, c = 1.0f, tem5 = 0.0f;
+  V2 eo1 = u, s = sp(0.0f), c = sp(1.0f), tem5 = sp(0.0f);
   const int kiter = KITER > 0 ? KITER : ((flags >> KEPLER_SHIFT) & 0xf);
 #pragma unroll
   for (int it = 0; it < (KITER > 0 ? KITER : 16); ++it) {
     if (KITER == 0 && it >= kiter) break;
-    sincos_a(eo1, s, c);
-    const float den = fmaf(-s, aynl, fmaf(-c, axnl, 1.0f));
-    const float num = fmaf(axnl, s, fmaf(-aynl, c, u)) - eo1;
-    tem5 = num * rcp_a(den);
+    sincos2(eo1, s, c);
+    const V2 den = fma2(-s, aynl, fma2(-c, axnl, 1.0f));
+    const V2 num = fma2(axnl, s, fma2(-aynl, c, u)) - eo1;
+    tem5 = num * rcp2(den);
     // the +-0.95 clamp (kernel.py:343-346) cannot trigger for e < 0.1
     // (|num| <= 2e, den >= 1 - 2e), i.e. for KITER 1 and 2
-    if (KITER == 0 || KITER > 2) tem5 = fminf(fmaxf(tem5, -0.95f), 0.95f);
-    eo1 += tem5;
+    if (KITER == 0 || KITER > 2) tem5 = clamp95(tem5);
+    eo1 = eo1 + tem5;
   }
-  float sineo1, coseo1;
+  V2 sineo1, coseo1;
   if constexpr (KITER > 0) {
     rotate_tiny(s, c, tem5, sineo1, coseo1);     // last step <= e^3/2 < 4e-3
   } else {
-    sincos_a(eo1, sineo1, coseo1);
+    sincos2(eo1, sineo1, coseo1);
   }
 
   // short-period preliminaries  kernel.py:440-460
-  const float ecose = fmaf(axnl, coseo1, aynl * sineo1);
-  const float esine = fmaf(axnl, sineo1, -aynl * coseo1);
-  const float el2 = fmaf(axnl, axnl, aynl * aynl);
-  const float pl = am * (1.0f - el2);
-  const bool bad_pl = pl < 0.0f;
-  const float pl_safe = fmaxf(pl, tiny);
-  const float rl = am * (1.0f - ecose);
-  const float irl = rcp_a(rl == 0.0f ? tiny : rl);
-  const float sqam = am * rsam;                           // sqrt(am)
-  const float rdotl = sqam * esine * irl;                 // sqrt(am) esine / rl
-  float rvdotl, betal, tq, ipl, sinu, cosu;
+  const V2 ecose = fma2(axnl, coseo1, aynl * sineo1);
+  const V2 esine = fma2(axnl, sineo1, (-aynl) * coseo1);
+  const V2 el2 = fma2(axnl, axnl, aynl * aynl);
+  const V2 pl = am * (1.0f - el2);
+  const bool bad_pl[2] = {pl.v.x < 0.0f, pl.v.y < 0.0f};
+  const V2 pl_safe = vmax(pl, tiny);
+  const V2 rl = am * (1.0f - ecose);
+  const V2 irl = rcp2({make_float2(rl.v.x == 0.0f ? tiny : rl.v.x, rl.v.y == 0.0f ? tiny : rl.v.y)});
+  const V2 sqam = am * rsam;                               // sqrt(am)
+  const V2 rdotl = sqam * esine * irl;                     // sqrt(am) esine / rl
+  V2 rvdotl, betal, tq, ipl;
   if constexpr (KITER == 1 || KITER == 2) {
     // e < 0.1 so x = el2 < 0.012: sqrt(1-x), 1/(1+sqrt(1-x)) and 1/(1-x)
     // as series in x (truncation < 1e-8 relative); pl > 0 here.
-    const float x = el2;
-    betal = fmaf(x, fmaf(x, fmaf(x, -0.0625f, -0.125f), -0.5f), 1.0f);
-    tq = esine * fmaf(x, fmaf(x, fmaf(x, 0.0390625f, 0.0625f), 0.125f), 0.5f);
-    rvdotl = sqam * betal * irl;                          // sqrt(am (1-x)) / rl
-    ipl = (rsam * rsam) * fmaf(x, fmaf(x, x + 1.0f, 1.0f), 1.0f);
+    const V2 x = el2;
+    betal = fma2(x, fma2(x, fma2(x, -0.0625f, -0.125f), -0.5f), 1.0f);
+    tq = esine * fma2(x, fma2(x, fma2(x, 0.0390625f, 0.0625f), 0.125f), 0.5f);
+    rvdotl = sqam * betal * irl;                           // sqrt(am (1-x)) / rl
+    ipl = (rsam * rsam) * fma2(x, fma2(x, x + 1.0f, 1.0f), 1.0f);
   } else {
-    const float rspl = rsq_a(pl_safe);
-    rvdotl = (pl_safe * rspl) * irl;                      // sqrt(pl) / rl
-    const float omel2 = fmaxf(1.0f - el2, tiny);
-    betal = omel2 * rsq_a(omel2);
-    tq = esine * rcp_a(1.0f + betal);
+    const V2 rspl = rsq2(pl_safe);
+    rvdotl = (pl_safe * rspl) * irl;                       // sqrt(pl) / rl
+    const V2 omel2 = vmax(1.0f - el2, tiny);
+    betal = omel2 * rsq2(omel2);
+    tq = esine * rcp2(betal + 1.0f);
     ipl = rspl * rspl;
   }
   // (sin u, cos u) = (am/rl) (sn, cs)  (kernel.py:453-454); the atan2 of
   // :455 is only ever used through sin/cos, so no angle is formed.
-  // |(sn, cs)| = rl/am is an identity in E, so am/rl is the exact norm.
-  {
-    const float sn = fmaf(-axnl, tq, sineo1 - aynl);
-    const float cs = fmaf(aynl, tq, coseo1 - axnl);
-    const float nrm = am * irl;
-    sinu = sn * nrm;
-    cosu = cs * nrm;
-  }
-  const float sin2u = (cosu + cosu) * sinu;
-  const float cos2u = fmaf(-2.0f * sinu, sinu, 1.0f);
-  const float temp1 = g.half_j2_f * ipl;
-  const float temp2 = temp1 * ipl;
+  const V2 nrm = am * irl;
+  const V2 sinu = fma2(-axnl, tq, sineo1 - aynl) * nrm;
+  const V2 cosu = fma2(aynl, tq, coseo1 - axnl) * nrm;
+  const V2 sin2u = (cosu + cosu) * sinu;
+  const V2 cos2u = fma2(sinu * -2.0f, sinu, 1.0f);
+  const V2 temp1 = ipl * g.half_j2_f;
+  const V2 temp2 = temp1 * ipl;
 
   // short-period periodics  kernel.py:463-469 (per-satellite factors
   // pre-multiplied in the record)
-  const float n15c41 = R.v[S32_NEG15CON41], x1mth2 = R.v[S_X1MTH2];
-  const float mrt = fmaf(rl, fmaf(n15c41 * temp2, betal, 1.0f),
-                         (temp1 * R.v[S32_HALFX1MTH2]) * cos2u);
-  const float t2s = temp2 * sin2u;
-  const float dsu = R.v[S32_QX7THM1] * t2s;
-  const float dinc = R.v[S32_C15COSSIN] * (temp2 * cos2u);
-  const float nmt = rsam3 * temp1;                          // nm temp1 / xke
-  const float mvt = fmaf(-nmt * x1mth2, sin2u, rdotl);
-  const float rvdot = fmaf(nmt, fmaf(x1mth2, cos2u, -n15c41), rvdotl);
+  const float n15c41 = R[S32_NEG15CON41], x1mth2 = R[S_X1MTH2];
+  const V2 mrt = fma2(rl, fma2(temp2 * n15c41, betal, 1.0f), (temp1 * R[S32_HALFX1MTH2]) * cos2u);
+  const V2 t2s = temp2 * sin2u;
+  const V2 dsu = t2s * R[S32_QX7THM1];
+  const V2 dinc = (temp2 * cos2u) * R[S32_C15COSSIN];
+  const V2 nmt = rsam3 * temp1;                            // nm temp1 / xke
+  const V2 mvt = fma2((-nmt) * x1mth2, sin2u, rdotl);
+  const V2 rvdot = fma2(nmt, fma2(cos2u, x1mth2, sp(-n15c41)), rvdotl);
 
   // orientation  kernel.py:472-493
-  float sinsu, cossu, snod, cnod, sini, cosi;
+  V2 sinsu, cossu, snod, cnod, sini, cosi;
   rotate_tiny(sinu, cosu, dsu, sinsu, cossu);
-  sincos_a(fmaf(R.v[S32_C15COSIO], t2s, nodem), snod, cnod);   // xnode
-  rotate_tiny(R.v[S_SINIO], R.v[S_COSIO], dinc, sini, cosi);
+  sincos2(fma2(t2s, R[S32_C15COSIO], nodem), snod, cnod);   // xnode
+  rotate_tiny(sp(R[S_SINIO]), sp(R[S_COSIO]), dinc, sini, cosi);
   // r = mr U, v = mv U + rv V with U, V the orientation vectors; grouped as
   // r = (xm, cnod|snod, sini) . (mr sinsu, mr cossu), same for v
-  const float xmx = -snod * cosi;
-  const float xmy = cnod * cosi;
-  const float mr = mrt * g.re_f;
-  const float ra = mr * sinsu, rb = mr * cossu;
-  o[0] = fmaf(xmx, ra, cnod * rb);
-  o[1] = fmaf(xmy, ra, snod * rb);
+  const V2 xmx = (-snod) * cosi;
+  const V2 xmy = cnod * cosi;
+  const V2 mr = mrt * g.re_f;
+  const V2 ra = mr * sinsu, rb = mr * cossu;
+  o[0] = fma2(xmx, ra, cnod * rb);
+  o[1] = fma2(xmy, ra, snod * rb);
   o[2] = sini * ra;
-  const float mv = mvt * g.vkm_f, rv = rvdot * g.vkm_f;
-  const float va = fmaf(mv, sinsu, rv * cossu);
-  const float vb = fmaf(mv, cossu, -rv * sinsu);
-  o[3] = fmaf(xmx, va, cnod * vb);
-  o[4] = fmaf(xmy, va, snod * vb);
+  const V2 mv = mvt * g.vkm_f, rv = rvdot * g.vkm_f;
+  const V2 va = fma2(mv, sinsu, rv * cossu);
+  const V2 vb = fma2(mv, cossu, (-rv) * sinsu);
+  o[3] = fma2(xmx, va, cnod * vb);
+  o[4] = fma2(xmy, va, snod * vb);
   o[5] = sini * va;
 
   // _first_error 2 > 1 > 4 > 6 and the init merge  kernel.py:497-502, 529-534
   const int persistent = (flags >> CODE_SHIFT) & 0xff;     // includes bad_nm -> 2
-  const int cellc = bad_em ? 1 : bad_pl ? 4 : (mrt < 1.0f) ? 6 : 0;
-  code = persistent != 0 ? persistent : cellc;
+  const float mrts[2] = {mrt.v.x, mrt.v.y};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (mrts[h] < 1.0f) ? 6 : 0;
+    code[h] = persistent != 0 ? persistent : cellc;
+  }
 }
 
 // ======================================================================
@@ -919,47 +965,61 @@ __device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
   if constexpr (N % 2) v[N - 1] = __ldg(p + N - 1);
 }
 
-template <bool ISIMP, int KITER>
-__device__ __forceinline__ void compute_n(const Rec<float>& R, const float (&th)[kCellsPerLane],
-                                         const float (&tl)[kCellsPerLane], const Grav& g,
-                                         float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
+static_assert(kCellsPerLane % 2 == 0, "fp32 cells run in pairs");
+
+template <bool ISIMP, int KITER, bool LO, class RT>
+__device__ __forceinline__ void compute_n(const RT& R, const float (&th)[kCellsPerLane],
+                                          const float (&tl)[kCellsPerLane], const Grav& g,
+                                          float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
 #pragma unroll
-  for (int k = 0; k < kCellsPerLane; ++k) {
-    float o[6];
-    cell32<ISIMP, KITER>(R, th[k], tl[k], g, o, code[k]);
+  for (int k = 0; k < kCellsPerLane; k += 2) {
+    V2 o[6];
+    int c2[2];
+    cell2<ISIMP, KITER, LO>(R, V2{make_float2(th[k], th[k + 1])}, V2{make_float2(tl[k], tl[k + 1])},
+                            g, o, c2);
 #pragma unroll
-    for (int p = 0; p < 6; ++p) out[p][k] = o[p];
+    for (int p = 0; p < 6; ++p) {
+      out[p][k] = o[p].v.x;
+      out[p][k + 1] = o[p].v.y;
+    }
+    code[k] = c2[0];
+    code[k + 1] = c2[1];
   }
 }
 
 // warp-uniform dispatch on the satellite's (isimp, Kepler count)
-__device__ __forceinline__ void compute_cells(const Rec<float>& R, const float (&th)[kCellsPerLane],
+template <bool LO, class RT>
+__device__ __forceinline__ void compute_cells(const RT& R, const float (&th)[kCellsPerLane],
                                               const float (&tl)[kCellsPerLane], const Grav& g,
                                               float (&out)[6][kCellsPerLane],
                                               int (&code)[kCellsPerLane]) {
   const int flags = R.flags();
   const int kit = (flags >> KEPLER_SHIFT) & 0xf;
   if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) compute_n<false, 1>(R, th, tl, g, out, code);
-    else if (kit == 2) compute_n<false, 2>(R, th, tl, g, out, code);
-    else if (kit == 3) compute_n<false, 3>(R, th, tl, g, out, code);
-    else compute_n<false, 0>(R, th, tl, g, out, code);
+    if (kit == 1) compute_n<false, 1, LO>(R, th, tl, g, out, code);
+    else if (kit == 2) compute_n<false, 2, LO>(R, th, tl, g, out, code);
+    else if (kit == 3) compute_n<false, 3, LO>(R, th, tl, g, out, code);
+    else compute_n<false, 0, LO>(R, th, tl, g, out, code);
   } else {
-    if (kit == 1) compute_n<true, 1>(R, th, tl, g, out, code);
-    else if (kit == 2) compute_n<true, 2>(R, th, tl, g, out, code);
-    else if (kit == 3) compute_n<true, 3>(R, th, tl, g, out, code);
-    else compute_n<true, 0>(R, th, tl, g, out, code);
+    if (kit == 1) compute_n<true, 1, LO>(R, th, tl, g, out, code);
+    else if (kit == 2) compute_n<true, 2, LO>(R, th, tl, g, out, code);
+    else if (kit == 3) compute_n<true, 3, LO>(R, th, tl, g, out, code);
+    else compute_n<true, 0, LO>(R, th, tl, g, out, code);
   }
 }
 
-__device__ __forceinline__ void compute_cells(const Rec<double>& R, const double (&th)[kCellsPerLane],
+template <bool LO, class RT>
+__device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kCellsPerLane],
                                               const float (&)[kCellsPerLane], const Grav& g,
                                               double (&out)[6][kCellsPerLane],
                                               int (&code)[kCellsPerLane]) {
+  Rec<double> RR;
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) RR.v[i] = R[i];
 #pragma unroll
   for (int k = 0; k < kCellsPerLane; ++k) {
     Cell64 c;
-    cell64(R, th[k], g, c);
+    cell64(RR, th[k], g, c);
     out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
     out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
     code[k] = c.code;
@@ -968,22 +1028,34 @@ __device__ __forceinline__ void compute_cells(const Rec<double>& R, const double
 
 // single cell with the same dispatch (pairs kernel): identical arithmetic
 // to the grid kernel's cells, so batch == scalar bit for bit
+template <bool ISIMP, int KITER, bool LO>
+__device__ __forceinline__ void one2(const Rec<float>& R, float th, float tl, const Grav& g,
+                                     float (&o)[6], int& code) {
+  V2 r[6];
+  int c2[2];
+  cell2<ISIMP, KITER, LO>(R, sp(th), sp(tl), g, r, c2);
+#pragma unroll
+  for (int p = 0; p < 6; ++p) o[p] = r[p].v.x;
+  code = c2[0];
+}
+template <bool LO>
 __device__ __forceinline__ void compute_one(const Rec<float>& R, float th, float tl, const Grav& g,
                                             float (&o)[6], int& code) {
   const int flags = R.flags();
   const int kit = (flags >> KEPLER_SHIFT) & 0xf;
   if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) cell32<false, 1>(R, th, tl, g, o, code);
-    else if (kit == 2) cell32<false, 2>(R, th, tl, g, o, code);
-    else if (kit == 3) cell32<false, 3>(R, th, tl, g, o, code);
-    else cell32<false, 0>(R, th, tl, g, o, code);
+    if (kit == 1) one2<false, 1, LO>(R, th, tl, g, o, code);
+    else if (kit == 2) one2<false, 2, LO>(R, th, tl, g, o, code);
+    else if (kit == 3) one2<false, 3, LO>(R, th, tl, g, o, code);
+    else one2<false, 0, LO>(R, th, tl, g, o, code);
   } else {
-    if (kit == 1) cell32<true, 1>(R, th, tl, g, o, code);
-    else if (kit == 2) cell32<true, 2>(R, th, tl, g, o, code);
-    else if (kit == 3) cell32<true, 3>(R, th, tl, g, o, code);
-    else cell32<true, 0>(R, th, tl, g, o, code);
+    if (kit == 1) one2<true, 1, LO>(R, th, tl, g, o, code);
+    else if (kit == 2) one2<true, 2, LO>(R, th, tl, g, o, code);
+    else if (kit == 3) one2<true, 3, LO>(R, th, tl, g, o, code);
+    else one2<true, 0, LO>(R, th, tl, g, o, code);
   }
 }
+template <bool LO>
 __device__ __forceinline__ void compute_one(const Rec<double>& R, double th, float, const Grav& g,
                                             double (&o)[6], int& code) {
   Cell64 c;
@@ -996,7 +1068,10 @@ __device__ __forceinline__ void compute_one(const Rec<double>& R, double th, flo
 // Persistent warps: the (satellite, 128-step chunk) work items of the grid
 // are split into one contiguous range per resident warp, so a warp reloads
 // its satellite record only when the range crosses a row.
-template <typename T, bool VEC>
+#ifndef SGP4B_SMEM_REC
+#define SGP4B_SMEM_REC 0
+#endif
+template <typename T, bool VEC, bool LO>
 __global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 1)
 grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
             const float* __restrict__ times_lo, int64_t m, Grav g, T* __restrict__ planes,
@@ -1012,8 +1087,22 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
   int64_t sat = g0 / chunks;
   int64_t chunk = g0 - sat * chunks;
 
+#if SGP4B_SMEM_REC
+  __shared__ __align__(16) T srec[kGridBlock / 32][S_COUNT];
+  T* my = srec[threadIdx.x >> 5];
+  auto fetch = [&](int64_t s_) {
+    __syncwarp();
+    const T* src = rec + s_ * S_COUNT;
+    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(src + i);
+    __syncwarp();
+  };
+  RecS<T> R{my};
+  fetch(sat);
+#else
   Rec<T> R;
-  load_rec(rec + sat * S_COUNT, R);
+  auto fetch = [&](int64_t s_) { load_rec(rec + s_ * S_COUNT, R); };
+  fetch(sat);
+#endif
   for (int64_t gi = g0; gi < g1; ++gi) {
     const int64_t j0 = chunk * kCellsPerWarp + lane * kCellsPerLane;
     if (j0 < m) {
@@ -1027,15 +1116,11 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
         for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
       }
 #pragma unroll
-      for (int k = 0; k < kCellsPerLane; ++k) tl[k] = 0.0f;
-      if (times_lo != nullptr) {
-#pragma unroll
-        for (int k = 0; k < kCellsPerLane; ++k) tl[k] = j0 + k < m ? __ldg(times_lo + j0 + k) : 0.0f;
-      }
+      for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
 
       T out[6][kCellsPerLane];
       int code[kCellsPerLane];
-      compute_cells(R, th, tl, g, out, code);
+      compute_cells<LO>(R, th, tl, g, out, code);
 
       T* base = planes + sat * row_stride + j0;
       int32_t* cbase = codes + sat * code_stride + j0;
@@ -1057,7 +1142,7 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
     if (++chunk == chunks) {
       chunk = 0;
       ++sat;
-      if (gi + 1 < g1) load_rec(rec + sat * S_COUNT, R);
+      if (gi + 1 < g1) fetch(sat);
     }
   }
 }
@@ -1076,7 +1161,10 @@ pairs_kernel(const T* __restrict__ rec, const int64_t* __restrict__ idx, const T
   load_rec(rec + idx[k] * S_COUNT, R);
   T o[6];
   int code;
-  compute_one(R, times[k], times_lo != nullptr ? times_lo[k] : 0.0f, g, o, code);
+  if (times_lo != nullptr)
+    compute_one<true>(R, times[k], times_lo[k], g, o, code);
+  else
+    compute_one<false>(R, times[k], 0.0f, g, o, code);
 #pragma unroll
   for (int q = 0; q < 6; ++q) rv[q * p + k] = o[q];
   codes[k] = code;
@@ -1117,8 +1205,8 @@ int64_t resident_blocks(int precision, bool vec) {
   int sms = 0, per_sm = 0;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const void* fn = precision == 64
-      ? (vec ? (const void*)grid_kernel<double, true> : (const void*)grid_kernel<double, false>)
-      : (vec ? (const void*)grid_kernel<float, true> : (const void*)grid_kernel<float, false>);
+      ? (vec ? (const void*)grid_kernel<double, true, false> : (const void*)grid_kernel<double, false, false>)
+      : (vec ? (const void*)grid_kernel<float, true, false> : (const void*)grid_kernel<float, false, false>);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridBlock, 0);
   if (e != cudaSuccess || sms <= 0 || per_sm <= 0) {
     fail(SGP4B_ECUDA, "occupancy query: %s", cudaGetErrorString(e));
@@ -1197,24 +1285,18 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_de
     const double* rec = static_cast<const double*>(record_dev);
     const double* t = static_cast<const double*>(times_dev);
     double* out = static_cast<double*>(planes_dev);
-    if (vec)
-      grid_kernel<double, true><<<(unsigned)blocks, kGridBlock, 0, s>>>(
-          rec, n, t, nullptr, m, g, out, plane_stride, row_stride, codes_dev, code_stride, chunks);
-    else
-      grid_kernel<double, false><<<(unsigned)blocks, kGridBlock, 0, s>>>(
-          rec, n, t, nullptr, m, g, out, plane_stride, row_stride, codes_dev, code_stride, chunks);
+    auto k = vec ? grid_kernel<double, true, false> : grid_kernel<double, false, false>;
+    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(rec, n, t, nullptr, m, g, out, plane_stride,
+                                              row_stride, codes_dev, code_stride, chunks);
   } else {
     const float* rec = static_cast<const float*>(record_dev);
     const float* t = static_cast<const float*>(times_dev);
     float* out = static_cast<float*>(planes_dev);
-    if (vec)
-      grid_kernel<float, true><<<(unsigned)blocks, kGridBlock, 0, s>>>(
-          rec, n, t, times_lo_dev, m, g, out, plane_stride, row_stride, codes_dev, code_stride,
-          chunks);
-    else
-      grid_kernel<float, false><<<(unsigned)blocks, kGridBlock, 0, s>>>(
-          rec, n, t, times_lo_dev, m, g, out, plane_stride, row_stride, codes_dev, code_stride,
-          chunks);
+    const bool lo = times_lo_dev != nullptr;
+    auto k = vec ? (lo ? grid_kernel<float, true, true> : grid_kernel<float, true, false>)
+                 : (lo ? grid_kernel<float, false, true> : grid_kernel<float, false, false>);
+    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(rec, n, t, times_lo_dev, m, g, out, plane_stride,
+                                              row_stride, codes_dev, code_stride, chunks);
   }
   return check_launch("sgp4b_propagate_grid");
 }
