@@ -241,6 +241,28 @@ struct Cell64 {
   int code;
 };
 
+// (sin, cos)(a + d) from (sin, cos)(a): series to d^7 / d^6 when
+// |d| < 2^-6 (truncation < 1e-19, below fp64 resolution of the result),
+// otherwise a direct sincos of the new angle `x`.
+__device__ __forceinline__ void rotate64(double s, double c, double d, double x, double& so,
+                                         double& co) {
+  if (fabs(d) < 0.015625) {
+    const double d2 = d * d;
+    const double sd = d * fma(d2, fma(d2, fma(d2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
+    const double cd = fma(d2, fma(d2, fma(d2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+    so = fma(s, cd, c * sd);
+    co = fma(c, cd, -s * sd);
+  } else {
+    sincos(x, &so, &co);
+  }
+}
+
+// fp64 cell.  Reference operation order and guards (kernel.py:352-510);
+// sin/cos are evaluated once per angle family: the drag correction of the
+// mean anomaly, the Newton updates of Kepler's E and the J2 short-period
+// corrections of su and xinc are applied as rotations (rotate64), and the
+// atan2 of kernel.py:455 is replaced by normalising (sin u, cos u) — only
+// sin/cos of su are ever used.  All of it is exact to fp64 rounding.
 __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Grav& g, Cell64& o) {
   const double tiny = DBL_MIN;
   const double xke = g.xke, j2 = g.j2, re = g.re;
@@ -249,34 +271,38 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   const bool isimp = flags & FLAG_ISIMP;
 
   // secular gravity and atmospheric drag  kernel.py:365-391
-  double xmdf = R.v[S_MO] + R.v[S_MDOT] * t;
-  double argpdf = R.v[S_ARGPO] + R.v[S_ARGPDOT] * t;
-  double nodedf = R.v[S_NODEO] + R.v[S_NODEDOT] * t;
-  double t2 = t * t;
+  const double xmdf = R.v[S_MO] + R.v[S_MDOT] * t;
+  const double argpdf = R.v[S_ARGPO] + R.v[S_ARGPDOT] * t;
+  const double nodedf = R.v[S_NODEO] + R.v[S_NODEDOT] * t;
+  const double t2 = t * t;
   double nodem = nodedf + R.v[S_NODECF] * t2;
   double tempa = 1.0 - R.v[S_CC1] * t;
   double tempe = R.v[S_BC4] * t;
   double templ = R.v[S_T2COF] * t2;
   double mm = xmdf, argpm = argpdf;
   if (!isimp) {
-    double delomg = R.v[S_OMGCOF] * t;
-    double delmtemp = 1.0 + R.v[S_ETA] * cos(xmdf);
-    double delm = R.v[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R.v[S_DELMO]);
-    double temp = delomg + delm;
+    double sx, cx;
+    sincos(xmdf, &sx, &cx);
+    const double delomg = R.v[S_OMGCOF] * t;
+    const double delmtemp = 1.0 + R.v[S_ETA] * cx;
+    const double delm = R.v[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R.v[S_DELMO]);
+    const double temp = delomg + delm;
     mm = xmdf + temp;
     argpm = argpdf - temp;
-    double t3 = t2 * t;
-    double t4 = t3 * t;
+    const double t3 = t2 * t;
+    const double t4 = t3 * t;
     tempa = tempa - R.v[S_D2] * t2 - R.v[S_D3] * t3 - R.v[S_D4] * t4;
-    tempe = tempe + R.v[S_BC5] * (sin(mm) - R.v[S_SINMAO]);
+    double smm, cmm;
+    rotate64(sx, cx, temp, mm, smm, cmm);                // sin(mm)
+    tempe = tempe + R.v[S_BC5] * (smm - R.v[S_SINMAO]);
     templ = templ + R.v[S_T3COF] * t3 + t4 * (R.v[S_T4COF] + t * R.v[S_T5COF]);
   }
 
   // mean motion / eccentricity update  kernel.py:393-414
-  const bool bad_nm = flags & FLAG_BAD_NM;
-  double am = R.v[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
-  double am_safe = gmax(am, tiny);
-  double nm = xke / pow(am_safe, 1.5);
+  const double am = R.v[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
+  const double am_safe = gmax(am, tiny);
+  const double sqam = sqrt(am_safe);
+  const double nm = xke / (am_safe * sqam);       // xke / am^1.5
   double em = R.v[S_ECCO] - tempe;
   const bool bad_em = (em >= 1.0) || (em < -0.001);
   em = em < 1.0e-6 ? 1.0e-6 : em;
@@ -291,77 +317,94 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   const double cosip = R.v[S_COSIO];
 
   // long-period periodics  kernel.py:419-431
-  double ep = em;
+  const double ep = em;
   double sa, ca;
   sincos(argpm, &sa, &ca);
-  double axnl = ep * ca;
-  double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
-  double temp = 1.0 / pl_lp;
-  double aynl = ep * sa + temp * R.v[S_AYCOF];
-  double xl = mm + argpm + nodem + temp * R.v[S_XLCOF] * axnl;
+  const double axnl = ep * ca;
+  const double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
+  const double ilp = 1.0 / pl_lp;
+  const double aynl = ep * sa + ilp * R.v[S_AYCOF];
+  const double xl = mm + argpm + nodem + ilp * R.v[S_XLCOF] * axnl;
 
-  // Kepler  kernel.py:434-437
-  double u = pymod_2pi(xl - nodem);
-  double eo1 = kepler_reference<double>(axnl, aynl, u);
-  double sineo1, coseo1;
-  sincos(eo1, &sineo1, &coseo1);
+  // Kepler  kernel.py:325-349, 434-437: (sin, cos) of E carried along the
+  // Newton updates by rotation
+  const double u = pymod_2pi(xl - nodem);
+  double eo1 = u, sineo1, coseo1;
+  sincos(u, &sineo1, &coseo1);
+  bool active = true;
+#pragma unroll 1
+  for (int it = 0; it < 10 && active; ++it) {
+    const double den = 1.0 - coseo1 * axnl - sineo1 * aynl;
+    double tem5 = (u - aynl * coseo1 + axnl * sineo1 - eo1) / den;
+    tem5 = tem5 >= 0.95 ? 0.95 : (tem5 <= -0.95 ? -0.95 : tem5);
+    eo1 = eo1 + tem5;
+    rotate64(sineo1, coseo1, tem5, eo1, sineo1, coseo1);
+    active = fabs(tem5) >= 1.0e-12;
+  }
 
   // short-period preliminaries  kernel.py:440-460
-  double ecose = axnl * coseo1 + aynl * sineo1;
-  double esine = axnl * sineo1 - aynl * coseo1;
-  double el2 = axnl * axnl + aynl * aynl;
-  double pl = am_safe * (1.0 - el2);
+  const double ecose = axnl * coseo1 + aynl * sineo1;
+  const double esine = axnl * sineo1 - aynl * coseo1;
+  const double el2 = axnl * axnl + aynl * aynl;
+  const double pl = am_safe * (1.0 - el2);
   const bool bad_pl = pl < 0.0;
-  double pl_safe = gmax(pl, tiny);
-  double rl = am_safe * (1.0 - ecose);
-  double rl_safe = rl == 0.0 ? tiny : rl;
-  double rdotl = sqrt(am_safe) * esine / rl_safe;
-  double rvdotl = sqrt(pl_safe) / rl_safe;
-  double betal = sqrt(gmax(1.0 - el2, tiny));
-  temp = esine / (1.0 + betal);
-  double sinu = am_safe / rl_safe * (sineo1 - aynl - axnl * temp);
-  double cosu = am_safe / rl_safe * (coseo1 - axnl + aynl * temp);
-  double su = atan2(sinu, cosu);
-  double sin2u = (cosu + cosu) * sinu;
-  double cos2u = 1.0 - 2.0 * sinu * sinu;
-  temp = 1.0 / pl_safe;
-  double temp1 = 0.5 * j2 * temp;
-  double temp2 = temp1 * temp;
+  const double pl_safe = gmax(pl, tiny);
+  const double rl = am_safe * (1.0 - ecose);
+  const double rl_safe = rl == 0.0 ? tiny : rl;
+  const double irl = 1.0 / rl_safe;
+  const double rdotl = sqam * esine * irl;
+  const double rvdotl = sqrt(pl_safe) * irl;
+  const double betal = sqrt(gmax(1.0 - el2, tiny));
+  const double tq = esine / (1.0 + betal);
+  // (sin u, cos u) normalised: the reference's am/rl factor is positive and
+  // only the direction reaches sin/cos(su)
+  const double sn = sineo1 - aynl - axnl * tq;
+  const double cs = coseo1 - axnl + aynl * tq;
+  const double inrm = rsqrt(sn * sn + cs * cs);
+  const double sinu = sn * inrm, cosu = cs * inrm;
+  const double sin2u = (cosu + cosu) * sinu;
+  const double cos2u = 1.0 - 2.0 * sinu * sinu;
+  const double ipl = 1.0 / pl_safe;
+  const double temp1 = 0.5 * j2 * ipl;
+  const double temp2 = temp1 * ipl;
 
   // short-period periodics  kernel.py:463-469
   const double con41 = R.v[S_CON41], x1mth2 = R.v[S_X1MTH2];
-  double mrt = rl * (1.0 - 1.5 * temp2 * betal * con41) + 0.5 * temp1 * x1mth2 * cos2u;
-  su = su - 0.25 * temp2 * R.v[S_X7THM1] * sin2u;
-  double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
-  double xinc = R.v[S_INCLO] + 1.5 * temp2 * cosip * sinip * cos2u;
-  double mvt = rdotl - nm * temp1 * x1mth2 * sin2u / xke;
-  double rvdot = rvdotl + nm * temp1 * (x1mth2 * cos2u + 1.5 * con41) / xke;
+  const double mrt = rl * (1.0 - 1.5 * temp2 * betal * con41) + 0.5 * temp1 * x1mth2 * cos2u;
+  const double dsu = -0.25 * temp2 * R.v[S_X7THM1] * sin2u;
+  const double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
+  const double dinc = 1.5 * temp2 * cosip * sinip * cos2u;
+  const double nmx = nm * temp1 / xke;
+  const double mvt = rdotl - nmx * x1mth2 * sin2u;
+  const double rvdot = rvdotl + nmx * (x1mth2 * cos2u + 1.5 * con41);
 
   // orientation  kernel.py:472-493
   double sinsu, cossu, snod, cnod, sini, cosi;
-  sincos(su, &sinsu, &cossu);
+  if (fabs(dsu) < 0.015625)
+    rotate64(sinu, cosu, dsu, 0.0, sinsu, cossu);
+  else
+    sincos(atan2(sinu, cosu) + dsu, &sinsu, &cossu);
   sincos(xnode, &snod, &cnod);
-  sincos(xinc, &sini, &cosi);
-  double xmx = -snod * cosi;
-  double xmy = cnod * cosi;
-  double ux = xmx * sinsu + cnod * cossu;
-  double uy = xmy * sinsu + snod * cossu;
-  double uz = sini * sinsu;
-  double vx = xmx * cossu - cnod * sinsu;
-  double vy = xmy * cossu - snod * sinsu;
-  double vz = sini * cossu;
-  double mr = mrt * re;
-  o.r[0] = mr * ux;
-  o.r[1] = mr * uy;
-  o.r[2] = mr * uz;
-  o.v[0] = (mvt * ux + rvdot * vx) * vkmpersec;
-  o.v[1] = (mvt * uy + rvdot * vy) * vkmpersec;
-  o.v[2] = (mvt * uz + rvdot * vz) * vkmpersec;
+  rotate64(sinip, cosip, dinc, R.v[S_INCLO] + dinc, sini, cosi);
+  const double xmx = -snod * cosi;
+  const double xmy = cnod * cosi;
+  const double mr = mrt * re;
+  const double ra = mr * sinsu, rb = mr * cossu;
+  o.r[0] = xmx * ra + cnod * rb;
+  o.r[1] = xmy * ra + snod * rb;
+  o.r[2] = sini * ra;
+  const double mv = mvt * vkmpersec, rv = rvdot * vkmpersec;
+  const double va = mv * sinsu + rv * cossu;
+  const double vb = mv * cossu - rv * sinsu;
+  o.v[0] = xmx * va + cnod * vb;
+  o.v[1] = xmy * va + snod * vb;
+  o.v[2] = sini * va;
 
-  // _first_error + init merge  kernel.py:495-502, 529-534
+  // _first_error + init merge  kernel.py:495-502, 529-534 (bad_nm is folded
+  // into the persistent code field of the record)
   const bool decayed = mrt < 1.0;
-  int code = bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
-  int persistent = (flags >> CODE_SHIFT) & 0xff;
+  const int code = bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
+  const int persistent = (flags >> CODE_SHIFT) & 0xff;
   o.code = persistent != 0 ? persistent : code;
 }
 
@@ -388,11 +431,9 @@ __device__ __forceinline__ V2 operator-(V2 a, V2 b) { return {__fadd2_rn(a.v, ma
 __device__ __forceinline__ V2 operator*(V2 a, V2 b) { return {__fmul2_rn(a.v, b.v)}; }
 __device__ __forceinline__ V2 fma2(V2 a, V2 b, V2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
 __device__ __forceinline__ V2 operator+(V2 a, float b) { return a + sp(b); }
-__device__ __forceinline__ V2 operator+(float a, V2 b) { return sp(a) + b; }
 __device__ __forceinline__ V2 operator-(float a, V2 b) { return sp(a) - b; }
 __device__ __forceinline__ V2 operator-(V2 a, float b) { return a - sp(b); }
 __device__ __forceinline__ V2 operator*(V2 a, float b) { return a * sp(b); }
-__device__ __forceinline__ V2 operator*(float a, V2 b) { return sp(a) * b; }
 __device__ __forceinline__ V2 fma2(V2 a, V2 b, float c) { return fma2(a, b, sp(c)); }
 __device__ __forceinline__ V2 fma2(V2 a, float b, V2 c) { return fma2(a, sp(b), c); }
 __device__ __forceinline__ V2 fma2(V2 a, float b, float c) { return fma2(a, sp(b), sp(c)); }
@@ -1016,7 +1057,9 @@ __device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kC
   Rec<double> RR;
 #pragma unroll
   for (int i = 0; i < S_COUNT; ++i) RR.v[i] = R[i];
-#pragma unroll
+  // one fp64 cell at a time: the fp64 pipe, not issue, is the limit, and
+  // keeping registers low doubles the resident warps
+#pragma unroll 1
   for (int k = 0; k < kCellsPerLane; ++k) {
     Cell64 c;
     cell64(RR, th[k], g, c);
@@ -1072,7 +1115,7 @@ __device__ __forceinline__ void compute_one(const Rec<double>& R, double th, flo
 #define SGP4B_SMEM_REC 0
 #endif
 template <typename T, bool VEC, bool LO>
-__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 1)
+__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 2)
 grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
             const float* __restrict__ times_lo, int64_t m, Grav g, T* __restrict__ planes,
             int64_t plane_stride, int64_t row_stride, int32_t* __restrict__ codes,
