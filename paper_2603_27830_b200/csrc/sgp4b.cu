@@ -421,22 +421,55 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
 // scalar API (pairs kernel) evaluates the same V2 code with both halves
 // equal and matches the grid bit for bit.
 
-struct V2 {
-  float2 v;
+// N cells (N even) as N/2 packed float2 halves; every op applies to all
+// halves in program order, so two cell-pairs advance in lockstep and the
+// scheduler always has an independent packed op in flight.
+template <int N>
+struct VN {
+  float2 h[N / 2];
 };
-__device__ __forceinline__ V2 sp(float s) { return {make_float2(s, s)}; }
-__device__ __forceinline__ V2 operator+(V2 a, V2 b) { return {__fadd2_rn(a.v, b.v)}; }
-__device__ __forceinline__ V2 operator-(V2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
-__device__ __forceinline__ V2 operator-(V2 a, V2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
-__device__ __forceinline__ V2 operator*(V2 a, V2 b) { return {__fmul2_rn(a.v, b.v)}; }
-__device__ __forceinline__ V2 fma2(V2 a, V2 b, V2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
-__device__ __forceinline__ V2 operator+(V2 a, float b) { return a + sp(b); }
-__device__ __forceinline__ V2 operator-(float a, V2 b) { return sp(a) - b; }
-__device__ __forceinline__ V2 operator-(V2 a, float b) { return a - sp(b); }
-__device__ __forceinline__ V2 operator*(V2 a, float b) { return a * sp(b); }
-__device__ __forceinline__ V2 fma2(V2 a, V2 b, float c) { return fma2(a, b, sp(c)); }
-__device__ __forceinline__ V2 fma2(V2 a, float b, V2 c) { return fma2(a, sp(b), c); }
-__device__ __forceinline__ V2 fma2(V2 a, float b, float c) { return fma2(a, sp(b), sp(c)); }
+template <int N>
+__device__ __forceinline__ VN<N> sp(float s) {
+  VN<N> r;
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) r.h[i] = make_float2(s, s);
+  return r;
+}
+#define VN_MAP1(expr)                      \
+  VN<N> r;                                 \
+  _Pragma("unroll") for (int i = 0; i < N / 2; ++i) r.h[i] = (expr); \
+  return r;
+template <int N>
+__device__ __forceinline__ VN<N> operator+(VN<N> a, VN<N> b) { VN_MAP1(__fadd2_rn(a.h[i], b.h[i])) }
+template <int N>
+__device__ __forceinline__ VN<N> operator-(VN<N> a) { VN_MAP1(make_float2(-a.h[i].x, -a.h[i].y)) }
+template <int N>
+__device__ __forceinline__ VN<N> operator-(VN<N> a, VN<N> b) {
+  VN_MAP1(__fadd2_rn(a.h[i], make_float2(-b.h[i].x, -b.h[i].y)))
+}
+template <int N>
+__device__ __forceinline__ VN<N> operator*(VN<N> a, VN<N> b) { VN_MAP1(__fmul2_rn(a.h[i], b.h[i])) }
+template <int N>
+__device__ __forceinline__ VN<N> fma2(VN<N> a, VN<N> b, VN<N> c) {
+  VN_MAP1(__ffma2_rn(a.h[i], b.h[i], c.h[i]))
+}
+template <int N>
+__device__ __forceinline__ VN<N> operator+(VN<N> a, float b) { return a + sp<N>(b); }
+template <int N>
+__device__ __forceinline__ VN<N> operator-(float a, VN<N> b) { return sp<N>(a) - b; }
+template <int N>
+__device__ __forceinline__ VN<N> operator-(VN<N> a, float b) { return a - sp<N>(b); }
+template <int N>
+__device__ __forceinline__ VN<N> operator*(VN<N> a, float b) { return a * sp<N>(b); }
+template <int N>
+__device__ __forceinline__ VN<N> fma2(VN<N> a, VN<N> b, float c) { return fma2(a, b, sp<N>(c)); }
+template <int N>
+__device__ __forceinline__ VN<N> fma2(VN<N> a, float b, VN<N> c) { return fma2(a, sp<N>(b), c); }
+template <int N>
+__device__ __forceinline__ VN<N> fma2(VN<N> a, float b, float c) { return fma2(a, sp<N>(b), sp<N>(c)); }
+// component k (0..N-1)
+template <int N>
+__device__ __forceinline__ float comp(const VN<N>& a, int k) { return (k & 1) ? a.h[k >> 1].y : a.h[k >> 1].x; }
 
 // SFU (MUFU) approximations with flush-to-zero, per component (sin/cos add
 // the FMUL by 1/2pi the SFU expects).  Absolute error of sin/cos ~2^-21 on
@@ -455,30 +488,51 @@ __device__ __forceinline__ void sincos_a(float x, float& s, float& c) {
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(x));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(x));
 }
-__device__ __forceinline__ V2 rcp2(V2 a) { return {make_float2(rcp_a(a.v.x), rcp_a(a.v.y))}; }
-__device__ __forceinline__ V2 rsq2(V2 a) { return {make_float2(rsq_a(a.v.x), rsq_a(a.v.y))}; }
-__device__ __forceinline__ void sincos2(V2 a, V2& s, V2& c) {
-  sincos_a(a.v.x, s.v.x, c.v.x);
-  sincos_a(a.v.y, s.v.y, c.v.y);
+template <int N>
+__device__ __forceinline__ VN<N> rcp2(VN<N> a) { VN_MAP1(make_float2(rcp_a(a.h[i].x), rcp_a(a.h[i].y))) }
+template <int N>
+__device__ __forceinline__ VN<N> rsq2(VN<N> a) { VN_MAP1(make_float2(rsq_a(a.h[i].x), rsq_a(a.h[i].y))) }
+template <int N>
+__device__ __forceinline__ void sincos2(VN<N> a, VN<N>& s, VN<N>& c) {
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    sincos_a(a.h[i].x, s.h[i].x, c.h[i].x);
+    sincos_a(a.h[i].y, s.h[i].y, c.h[i].y);
+  }
 }
-__device__ __forceinline__ V2 rint2(V2 a) { return {make_float2(rintf(a.v.x), rintf(a.v.y))}; }
+template <int N>
+__device__ __forceinline__ VN<N> rint2(VN<N> a) { VN_MAP1(make_float2(rintf(a.h[i].x), rintf(a.h[i].y))) }
 // maximum(x, f) == where(x >= f, x, f): fmaxf has the same NaN behaviour
-__device__ __forceinline__ V2 vmax(V2 a, float f) { return {make_float2(fmaxf(a.v.x, f), fmaxf(a.v.y, f))}; }
-__device__ __forceinline__ V2 clamp95(V2 a) {
-  return {make_float2(fminf(fmaxf(a.v.x, -0.95f), 0.95f), fminf(fmaxf(a.v.y, -0.95f), 0.95f))};
+template <int N>
+__device__ __forceinline__ VN<N> vmax(VN<N> a, float f) {
+  VN_MAP1(make_float2(fmaxf(a.h[i].x, f), fmaxf(a.h[i].y, f)))
+}
+template <int N>
+__device__ __forceinline__ VN<N> clamp95(VN<N> a) {
+  VN_MAP1(make_float2(fminf(fmaxf(a.h[i].x, -0.95f), 0.95f), fminf(fmaxf(a.h[i].y, -0.95f), 0.95f)))
+}
+// x < f ? f : x  (the em floor of kernel.py:406; NaN propagates)
+template <int N>
+__device__ __forceinline__ VN<N> floor_sel(VN<N> a, float f) {
+  VN_MAP1(make_float2(a.h[i].x < f ? f : a.h[i].x, a.h[i].y < f ? f : a.h[i].y))
+}
+// x == 0 ? tiny : x
+template <int N>
+__device__ __forceinline__ VN<N> nonzero(VN<N> a, float tiny) {
+  VN_MAP1(make_float2(a.h[i].x == 0.0f ? tiny : a.h[i].x, a.h[i].y == 0.0f ? tiny : a.h[i].y))
 }
 
 // x0 + (rate_hi + rate_lo) * (t + tl), reduced mod 2*pi, in double-float:
 // p = rate_hi*t rounded, its exact error by fma, k = nearest revolution;
 // p - k*2pi_hi is exact (the difference needs < 24 bits: DESIGN.md §4).
-template <bool LO>
-__device__ __forceinline__ V2 secular_angle(float x0, float rate, float rate_lo, V2 t, V2 tl) {
-  const V2 p = t * rate;
-  V2 e = fma2(t, rate, -p);
+template <bool LO, int N>
+__device__ __forceinline__ VN<N> secular_angle(float x0, float rate, float rate_lo, VN<N> t, VN<N> tl) {
+  const VN<N> p = t * rate;
+  VN<N> e = fma2(t, rate, -p);
   e = fma2(t, rate_lo, e);
   if constexpr (LO) e = fma2(tl, rate, e);
-  const V2 k = rint2(p * kInvTwoPiF);
-  V2 r = fma2(-k, kTwoPiHiF, p);
+  const VN<N> k = rint2(p * kInvTwoPiF);
+  VN<N> r = fma2(-k, kTwoPiHiF, p);
   r = fma2(-k, kTwoPiLoF, r);
   return r + (e + x0);
 }
@@ -486,8 +540,9 @@ __device__ __forceinline__ V2 secular_angle(float x0, float rate, float rate_lo,
 // (sin, cos)(a + d) from (sin, cos)(a) for |d| < 4e-3 (the J2 short-period
 // corrections and the last Newton step): d^3/6 < 1.1e-8 is below fp32
 // resolution, so sin d = d, cos d = 1 - d^2/2.
-__device__ __forceinline__ void rotate_tiny(V2 s, V2 c, V2 d, V2& so, V2& co) {
-  const V2 cd = fma2(d * d, -0.5f, 1.0f);
+template <int N>
+__device__ __forceinline__ void rotate_tiny(VN<N> s, VN<N> c, VN<N> d, VN<N>& so, VN<N>& co) {
+  const VN<N> cd = fma2(d * d, -0.5f, 1.0f);
   so = fma2(s, cd, c * d);
   co = fma2(c, cd, (-s) * d);
 }
@@ -496,31 +551,32 @@ __device__ __forceinline__ void rotate_tiny(V2 s, V2 c, V2 d, V2& so, V2& co) {
 // satellite and compile-time here, so the cell is straight-line code.
 // KITER = 0: runtime Kepler count with a final SFU sincos (eccentric
 // orbits).  `R[i]` is the satellite's packed record (scalar fields).
-template <bool ISIMP, int KITER, bool LO, class RT>
-__device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V2 (&o)[6],
-                                      int (&code)[2]) {
+template <bool ISIMP, int KITER, bool LO, int NC, class RT>
+__device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Grav& g,
+                                      VN<NC> (&o)[6], int (&code)[NC]) {
+  using V2 = VN<NC>;
   const float tiny = FLT_MIN;
   const int flags = R.flags();
 
   // secular gravity  kernel.py:366-370.  Only the Kepler argument needs the
   // double-float treatment: u = (mo + argpo) + (mdot + argpdot) t + ...
   // (mm + argpm; the drag term cancels), the rest enter sin/cos damped.
-  const V2 xmdf = fma2(t, R[S_MDOT], sp(R[S_MO]));
-  const V2 argpdf = fma2(t, R[S_ARGPDOT], sp(R[S_ARGPO]));
+  const V2 xmdf = fma2(t, R[S_MDOT], sp<NC>(R[S_MO]));
+  const V2 argpdf = fma2(t, R[S_ARGPDOT], sp<NC>(R[S_ARGPO]));
   const V2 t2 = t * t;
-  const V2 nodem = fma2(t2, R[S_NODECF], fma2(t, R[S_NODEDOT], sp(R[S_NODEO])));
-  const V2 ubase = secular_angle<LO>(R[S_U0], R[S_UDOT], R[S_UDOT_LO], t, tl);
+  const V2 nodem = fma2(t2, R[S_NODECF], fma2(t, R[S_NODEDOT], sp<NC>(R[S_NODEO])));
+  const V2 ubase = secular_angle<LO, NC>(R[S_U0], R[S_UDOT], R[S_UDOT_LO], t, tl);
 
   // drag  kernel.py:371-391
   V2 tempa = fma2(t, -R[S_CC1], 1.0f);
   V2 tempe = t * R[S_BC4];
   V2 templ = t2 * R[S_T2COF];
-  V2 temp = sp(0.0f);
+  V2 temp = sp<NC>(0.0f);
   if constexpr (!ISIMP) {
     V2 sx, cx;
     sincos2(xmdf, sx, cx);
     const V2 dmt = fma2(cx, R[S_ETA], 1.0f);
-    const V2 delm = fma2(dmt * dmt, dmt, sp(-R[S_DELMO])) * R[S_XMCOF];
+    const V2 delm = fma2(dmt * dmt, dmt, sp<NC>(-R[S_DELMO])) * R[S_XMCOF];
     temp = fma2(t, R[S_OMGCOF], delm);
     const V2 t3 = t2 * t;
     const V2 t4 = t2 * t2;
@@ -529,7 +585,7 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
     // (its square, times B* cc5, is far below fp32 resolution of em)
     const V2 smm = fma2(cx, temp, sx);
     tempe = fma2(smm - R[S_SINMAO], R[S_BC5], tempe);
-    templ = fma2(t4, fma2(t, R[S_T5COF], sp(R[S_T4COF])), fma2(t3, R[S_T3COF], templ));
+    templ = fma2(t4, fma2(t, R[S_T5COF], sp<NC>(R[S_T4COF])), fma2(t3, R[S_T3COF], templ));
   }
   const V2 argpm = argpdf - temp;
 
@@ -538,11 +594,10 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
   const V2 rsam = rsq2(am);
   const V2 rsam3 = rsam * rsam * rsam;                        // nm / xke = am^-1.5
   V2 em = R[S_ECCO] - tempe;
-  bool bad_em[2];
-  bad_em[0] = (em.v.x >= 1.0f) || (em.v.x < -0.001f);
-  bad_em[1] = (em.v.y >= 1.0f) || (em.v.y < -0.001f);
-  em.v.x = em.v.x < 1.0e-6f ? 1.0e-6f : em.v.x;
-  em.v.y = em.v.y < 1.0e-6f ? 1.0e-6f : em.v.y;
+  bool bad_em[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) bad_em[k] = (comp(em, k) >= 1.0f) || (comp(em, k) < -0.001f);
+  em = floor_sel(em, 1.0e-6f);
 
   // long-period periodics  kernel.py:420-431
   V2 sa, ca;
@@ -554,7 +609,7 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
   const V2 u = fma2(ilp * R[S_XLCOF], axnl, fma2(templ, R[S_NO], ubase));
 
   // Kepler, fixed warp-uniform iteration count  kernel.py:325-349
-  V2 eo1 = u, s = sp(0.0f), c = sp(1.0f), tem5 = sp(0.0f);
+  V2 eo1 = u, s = sp<NC>(0.0f), c = sp<NC>(1.0f), tem5 = sp<NC>(0.0f);
   const int kiter = KITER > 0 ? KITER : ((flags >> KEPLER_SHIFT) & 0xf);
 #pragma unroll
   for (int it = 0; it < (KITER > 0 ? KITER : 16); ++it) {
@@ -580,10 +635,12 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
   const V2 esine = fma2(axnl, sineo1, (-aynl) * coseo1);
   const V2 el2 = fma2(axnl, axnl, aynl * aynl);
   const V2 pl = am * (1.0f - el2);
-  const bool bad_pl[2] = {pl.v.x < 0.0f, pl.v.y < 0.0f};
+  bool bad_pl[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) bad_pl[k] = comp(pl, k) < 0.0f;
   const V2 pl_safe = vmax(pl, tiny);
   const V2 rl = am * (1.0f - ecose);
-  const V2 irl = rcp2({make_float2(rl.v.x == 0.0f ? tiny : rl.v.x, rl.v.y == 0.0f ? tiny : rl.v.y)});
+  const V2 irl = rcp2(nonzero(rl, tiny));
   const V2 sqam = am * rsam;                               // sqrt(am)
   const V2 rdotl = sqam * esine * irl;                     // sqrt(am) esine / rl
   V2 rvdotl, betal, tq, ipl;
@@ -622,13 +679,13 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
   const V2 dinc = (temp2 * cos2u) * R[S32_C15COSSIN];
   const V2 nmt = rsam3 * temp1;                            // nm temp1 / xke
   const V2 mvt = fma2((-nmt) * x1mth2, sin2u, rdotl);
-  const V2 rvdot = fma2(nmt, fma2(cos2u, x1mth2, sp(-n15c41)), rvdotl);
+  const V2 rvdot = fma2(nmt, fma2(cos2u, x1mth2, sp<NC>(-n15c41)), rvdotl);
 
   // orientation  kernel.py:472-493
   V2 sinsu, cossu, snod, cnod, sini, cosi;
   rotate_tiny(sinu, cosu, dsu, sinsu, cossu);
   sincos2(fma2(t2s, R[S32_C15COSIO], nodem), snod, cnod);   // xnode
-  rotate_tiny(sp(R[S_SINIO]), sp(R[S_COSIO]), dinc, sini, cosi);
+  rotate_tiny(sp<NC>(R[S_SINIO]), sp<NC>(R[S_COSIO]), dinc, sini, cosi);
   // r = mr U, v = mv U + rv V with U, V the orientation vectors; grouped as
   // r = (xm, cnod|snod, sini) . (mr sinsu, mr cossu), same for v
   const V2 xmx = (-snod) * cosi;
@@ -647,10 +704,9 @@ __device__ __forceinline__ void cell2(const RT& R, V2 t, V2 tl, const Grav& g, V
 
   // _first_error 2 > 1 > 4 > 6 and the init merge  kernel.py:497-502, 529-534
   const int persistent = (flags >> CODE_SHIFT) & 0xff;     // includes bad_nm -> 2
-  const float mrts[2] = {mrt.v.x, mrt.v.y};
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (mrts[h] < 1.0f) ? 6 : 0;
+  for (int h = 0; h < NC; ++h) {
+    const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (comp(mrt, h) < 1.0f) ? 6 : 0;
     code[h] = persistent != 0 ? persistent : cellc;
   }
 }
@@ -957,7 +1013,10 @@ __global__ void pack_kernel(const double* __restrict__ satrec, const int32_t* __
 #endif
 constexpr int kCellsPerLane = SGP4B_CELLS;          // consecutive time steps per lane
 constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // one work item (chunk)
-constexpr int kGridBlock = 256;
+#ifndef SGP4B_BLOCK
+#define SGP4B_BLOCK 256
+#endif
+constexpr int kGridBlock = SGP4B_BLOCK;
 constexpr int kGridMinBlocks = SGP4B_MINB;   // resident 256-thread blocks per SM (fp32)
 
 __device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
@@ -1006,25 +1065,32 @@ __device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
   if constexpr (N % 2) v[N - 1] = __ldg(p + N - 1);
 }
 
-static_assert(kCellsPerLane % 2 == 0, "fp32 cells run in pairs");
+#ifndef SGP4B_VEC
+#define SGP4B_VEC 4
+#endif
+constexpr int kVec = SGP4B_VEC;     // cells advanced in lockstep (2 = one packed pair)
+static_assert(kCellsPerLane % kVec == 0 && kVec % 2 == 0, "fp32 cells run in packed pairs");
 
 template <bool ISIMP, int KITER, bool LO, class RT>
 __device__ __forceinline__ void compute_n(const RT& R, const float (&th)[kCellsPerLane],
                                           const float (&tl)[kCellsPerLane], const Grav& g,
                                           float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
 #pragma unroll
-  for (int k = 0; k < kCellsPerLane; k += 2) {
-    V2 o[6];
-    int c2[2];
-    cell2<ISIMP, KITER, LO>(R, V2{make_float2(th[k], th[k + 1])}, V2{make_float2(tl[k], tl[k + 1])},
-                            g, o, c2);
+  for (int k = 0; k < kCellsPerLane; k += kVec) {
+    VN<kVec> tv, tlv, o[6];
+    int cv[kVec];
 #pragma unroll
-    for (int p = 0; p < 6; ++p) {
-      out[p][k] = o[p].v.x;
-      out[p][k + 1] = o[p].v.y;
+    for (int i = 0; i < kVec / 2; ++i) {
+      tv.h[i] = make_float2(th[k + 2 * i], th[k + 2 * i + 1]);
+      tlv.h[i] = make_float2(tl[k + 2 * i], tl[k + 2 * i + 1]);
     }
-    code[k] = c2[0];
-    code[k + 1] = c2[1];
+    cellv<ISIMP, KITER, LO, kVec>(R, tv, tlv, g, o, cv);
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+#pragma unroll
+      for (int p = 0; p < 6; ++p) out[p][k + j] = comp(o[p], j);
+      code[k + j] = cv[j];
+    }
   }
 }
 
@@ -1074,11 +1140,11 @@ __device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kC
 template <bool ISIMP, int KITER, bool LO>
 __device__ __forceinline__ void one2(const Rec<float>& R, float th, float tl, const Grav& g,
                                      float (&o)[6], int& code) {
-  V2 r[6];
+  VN<2> r[6];
   int c2[2];
-  cell2<ISIMP, KITER, LO>(R, sp(th), sp(tl), g, r, c2);
+  cellv<ISIMP, KITER, LO, 2>(R, sp<2>(th), sp<2>(tl), g, r, c2);
 #pragma unroll
-  for (int p = 0; p < 6; ++p) o[p] = r[p].v.x;
+  for (int p = 0; p < 6; ++p) o[p] = r[p].h[0].x;
   code = c2[0];
 }
 template <bool LO>
