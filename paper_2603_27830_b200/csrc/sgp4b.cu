@@ -567,25 +567,29 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 nodem = fma2(t2, R[S_NODECF], fma2(t, R[S_NODEDOT], sp<NC>(R[S_NODEO])));
   const V2 ubase = secular_angle<LO, NC>(R[S_U0], R[S_UDOT], R[S_UDOT_LO], t, tl);
 
-  // drag  kernel.py:371-391
-  V2 tempa = fma2(t, -R[S_CC1], 1.0f);
+  // drag  kernel.py:371-391; the t-polynomials in Horner form
+  V2 tempa, templ;
   V2 tempe = t * R[S_BC4];
-  V2 templ = t2 * R[S_T2COF];
   V2 temp = sp<NC>(0.0f);
-  if constexpr (!ISIMP) {
+  if constexpr (ISIMP) {
+    tempa = fma2(t, -R[S_CC1], 1.0f);
+    templ = t2 * R[S_T2COF];
+  } else {
     V2 sx, cx;
     sincos2(xmdf, sx, cx);
     const V2 dmt = fma2(cx, R[S_ETA], 1.0f);
     const V2 delm = fma2(dmt * dmt, dmt, sp<NC>(-R[S_DELMO])) * R[S_XMCOF];
     temp = fma2(t, R[S_OMGCOF], delm);
-    const V2 t3 = t2 * t;
-    const V2 t4 = t2 * t2;
-    tempa = fma2(t4, -R[S_D4], fma2(t3, -R[S_D3], fma2(t2, -R[S_D2], tempa)));
+    // 1 - cc1 t - d2 t^2 - d3 t^3 - d4 t^4
+    tempa = fma2(t, fma2(t, fma2(t, fma2(t, -R[S_D4], -R[S_D3]), sp<NC>(-R[S_D2])),
+                         sp<NC>(-R[S_CC1])), 1.0f);
+    // t2cof t^2 + t3cof t^3 + t4cof t^4 + t5cof t^5
+    templ = t2 * fma2(t, fma2(t, fma2(t, R[S_T5COF], R[S_T4COF]), sp<NC>(R[S_T3COF])),
+                      sp<NC>(R[S_T2COF]));
     // sin(xmdf + temp), temp the small drag correction of the mean anomaly
     // (its square, times B* cc5, is far below fp32 resolution of em)
     const V2 smm = fma2(cx, temp, sx);
     tempe = fma2(smm - R[S_SINMAO], R[S_BC5], tempe);
-    templ = fma2(t4, fma2(t, R[S_T5COF], sp<NC>(R[S_T4COF])), fma2(t3, R[S_T3COF], templ));
   }
   const V2 argpm = argpdf - temp;
 
@@ -644,7 +648,10 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 sqam = am * rsam;                               // sqrt(am)
   const V2 rdotl = sqam * esine * irl;                     // sqrt(am) esine / rl
   V2 rvdotl, betal, tq, ipl;
-  if constexpr (KITER == 1 || KITER == 2) {
+#ifndef SGP4B_SERIES
+#define SGP4B_SERIES 0
+#endif
+  if constexpr (SGP4B_SERIES && (KITER == 1 || KITER == 2)) {
     // e < 0.1 so x = el2 < 0.012: sqrt(1-x), 1/(1+sqrt(1-x)) and 1/(1-x)
     // as series in x (truncation < 1e-8 relative); pl > 0 here.
     const V2 x = el2;
