@@ -1181,9 +1181,98 @@ __device__ __forceinline__ void compute_one(const Rec<double>& R, double th, flo
   code = c.code;
 }
 
-// Persistent warps: the (satellite, 128-step chunk) work items of the grid
-// are split into one contiguous range per resident warp, so a warp reloads
-// its satellite record only when the range crosses a row.
+// One satellite row, chunks [c0, c1): per lane kCellsPerLane consecutive
+// steps per chunk.  CellsFn(th, tl, out, code) evaluates a lane's cells;
+// it is specialised per satellite class, so the chunk loop is branch-free.
+template <typename T, bool VEC, bool LO, class CellsFn>
+__device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64_t c1, int lane,
+                                         const T* __restrict__ times,
+                                         const float* __restrict__ times_lo, int64_t m,
+                                         T* __restrict__ row, int64_t plane_stride,
+                                         int32_t* __restrict__ crow) {
+  int64_t j0 = c0 * kCellsPerWarp + lane * kCellsPerLane;
+  for (int64_t c = c0; c < c1; ++c, j0 += kCellsPerWarp) {
+    if (j0 >= m) break;                     // only the row's last chunk is partial
+    T th[kCellsPerLane];
+    float tl[kCellsPerLane];
+    const bool full = j0 + kCellsPerLane <= m;
+    if (VEC && full) {
+      ld_vec<kCellsPerLane>(times + j0, th);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
+
+    T out[6][kCellsPerLane];
+    int code[kCellsPerLane];
+    cells(th, tl, out, code);
+
+    T* base = row + j0;
+    int32_t* cbase = crow + j0;
+    if (VEC && full) {
+#pragma unroll
+      for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
+      st_vec_cs<kCellsPerLane>(cbase, code);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) {
+        if (j0 + k < m) {
+#pragma unroll
+          for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
+          st_cs(cbase + k, code[k]);
+        }
+      }
+    }
+  }
+}
+
+template <bool ISIMP, int KITER, bool VEC, bool LO, class RT>
+__device__ __forceinline__ void row32(const RT& R, const Grav& g, int64_t c0, int64_t c1, int lane,
+                                      const float* times, const float* times_lo, int64_t m,
+                                      float* row, int64_t plane_stride, int32_t* crow) {
+  auto cells = [&](const float (&th)[kCellsPerLane], const float (&tl)[kCellsPerLane],
+                   float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
+    compute_n<ISIMP, KITER, LO>(R, th, tl, g, out, code);
+  };
+  row_loop<float, VEC, LO>(cells, c0, c1, lane, times, times_lo, m, row, plane_stride, crow);
+}
+
+// per-row dispatch on the satellite's (isimp, Kepler count): warp-uniform
+template <bool VEC, bool LO, class RT>
+__device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t c0, int64_t c1,
+                                             int lane, const float* times, const float* times_lo,
+                                             int64_t m, float* row, int64_t ps, int32_t* crow) {
+  const int flags = R.flags();
+  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
+  if (!(flags & FLAG_ISIMP)) {
+    if (kit == 1) row32<false, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else if (kit == 2) row32<false, 2, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else if (kit == 3) row32<false, 3, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else row32<false, 0, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  } else {
+    if (kit == 1) row32<true, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else if (kit == 2) row32<true, 2, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else if (kit == 3) row32<true, 3, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    else row32<true, 0, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  }
+}
+
+template <bool VEC, bool LO, class RT>
+__device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t c0, int64_t c1,
+                                             int lane, const double* times, const float* times_lo,
+                                             int64_t m, double* row, int64_t ps, int32_t* crow) {
+  auto cells = [&](const double (&th)[kCellsPerLane], const float (&tl)[kCellsPerLane],
+                   double (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
+    compute_cells<LO>(R, th, tl, g, out, code);
+  };
+  row_loop<double, VEC, LO>(cells, c0, c1, lane, times, times_lo, m, row, ps, crow);
+}
+
+// Persistent warps: the (satellite, chunk) work items of the grid are split
+// into one contiguous range per resident warp; the warp walks it row by row,
+// loading each satellite's record once and dispatching its class once.
 #ifndef SGP4B_SMEM_REC
 #define SGP4B_SMEM_REC 0
 #endif
@@ -1199,67 +1288,28 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
   const int64_t total = n * chunks;
   const int64_t g0 = total * w / nwarps;
   const int64_t g1 = total * (w + 1) / nwarps;
-  if (g0 >= g1) return;
-  int64_t sat = g0 / chunks;
-  int64_t chunk = g0 - sat * chunks;
 
 #if SGP4B_SMEM_REC
   __shared__ __align__(16) T srec[kGridBlock / 32][S_COUNT];
   T* my = srec[threadIdx.x >> 5];
-  auto fetch = [&](int64_t s_) {
-    __syncwarp();
-    const T* src = rec + s_ * S_COUNT;
-    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(src + i);
-    __syncwarp();
-  };
   RecS<T> R{my};
-  fetch(sat);
 #else
   Rec<T> R;
-  auto fetch = [&](int64_t s_) { load_rec(rec + s_ * S_COUNT, R); };
-  fetch(sat);
 #endif
-  for (int64_t gi = g0; gi < g1; ++gi) {
-    const int64_t j0 = chunk * kCellsPerWarp + lane * kCellsPerLane;
-    if (j0 < m) {
-      T th[kCellsPerLane];
-      float tl[kCellsPerLane];
-      const bool full = j0 + kCellsPerLane <= m;
-      if (VEC && full) {
-        ld_vec<kCellsPerLane>(times + j0, th);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
-      }
-#pragma unroll
-      for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
-
-      T out[6][kCellsPerLane];
-      int code[kCellsPerLane];
-      compute_cells<LO>(R, th, tl, g, out, code);
-
-      T* base = planes + sat * row_stride + j0;
-      int32_t* cbase = codes + sat * code_stride + j0;
-      if (VEC && full) {
-#pragma unroll
-        for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
-        st_vec_cs<kCellsPerLane>(cbase, code);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kCellsPerLane; ++k) {
-          if (j0 + k < m) {
-#pragma unroll
-            for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
-            st_cs(cbase + k, code[k]);
-          }
-        }
-      }
-    }
-    if (++chunk == chunks) {
-      chunk = 0;
-      ++sat;
-      if (gi + 1 < g1) fetch(sat);
-    }
+  for (int64_t gi = g0; gi < g1;) {
+    const int64_t sat = gi / chunks;
+    const int64_t c0 = gi - sat * chunks;
+    const int64_t c1 = (g1 - gi < chunks - c0) ? c0 + (g1 - gi) : chunks;
+#if SGP4B_SMEM_REC
+    __syncwarp();
+    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + sat * S_COUNT + i);
+    __syncwarp();
+#else
+    load_rec(rec + sat * S_COUNT, R);
+#endif
+    dispatch_row<VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, planes + sat * row_stride,
+                          plane_stride, codes + sat * code_stride);
+    gi += c1 - c0;
   }
 }
 
