@@ -86,6 +86,15 @@ int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev,
                           int64_t p, int precision, const double* grav,
                           void* rv_dev, int32_t* codes_dev, void* stream);
 
+/* fp32-vs-fp64 drift: per-cell |r32 - r64| (km) and |v32 - v64| (km/s) in
+ * fp64 for cells whose codes are 0 in both grids, +inf elsewhere.  Both
+ * grids contiguous (6, n, m); dr/dv (n, m).  Replaces the norm step of
+ * drift_report (drift.py:64-70); percentiles are taken by the caller. */
+int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
+                      const int32_t* codes32_dev, const int32_t* codes64_dev,
+                      int64_t n, int64_t m, double* dr_dev, double* dv_dev,
+                      void* stream);
+
 /* Newton solve of SGP4's Kepler equation, elementwise (kernel.py:325-349). */
 int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev,
                        const void* u_dev, int64_t n, int precision,

@@ -24,6 +24,7 @@ EXPORTED_SYMBOLS = (
     "sgp4b_pack",
     "sgp4b_propagate_grid",
     "sgp4b_propagate_pairs",
+    "sgp4b_drift_norms",
     "sgp4b_solve_kepler",
     "sgp4b_last_error",
     "sgp4b_abi_version",
@@ -40,6 +41,7 @@ _SIGNATURES = {
                                       _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
     "sgp4b_propagate_pairs": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp,
                                        _vp, _vp, _vp]),
+    "sgp4b_drift_norms": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
     "sgp4b_solve_kepler": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _vp, _vp]),
     "sgp4b_last_error": (ctypes.c_char_p, []),
     "sgp4b_abi_version": (_c_int, []),

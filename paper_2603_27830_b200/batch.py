@@ -158,6 +158,10 @@ def _times(sats: SatBatch, times) -> np.ndarray:
 
 
 def _alloc_grid(n: int, m: int, precision: int, device, pin: bool = False):
+    """Output grid.  On the device, rows are padded to a multiple of 4 steps
+    (returned as (6, n, m) / (n, m) views) so the grid kernel always runs its
+    vectorised instance — the one the scalar API shares, which keeps
+    batch == scalar bit for bit."""
     tdt = _device.torch_dtype(precision)
     itemsize = 4 if precision == 32 else 8
     try:
@@ -165,8 +169,9 @@ def _alloc_grid(n: int, m: int, precision: int, device, pin: bool = False):
             planes = torch.empty((6, n, m), dtype=tdt, pin_memory=pin)
             error = torch.empty((n, m), dtype=torch.int32, pin_memory=pin)
         else:
-            planes = torch.empty((6, n, m), dtype=tdt, device=device)
-            error = torch.empty((n, m), dtype=torch.int32, device=device)
+            m4 = -(-m // 4) * 4
+            planes = torch.empty((6, n, m4), dtype=tdt, device=device)[:, :, :m]
+            error = torch.empty((n, m4), dtype=torch.int32, device=device)[:, :m]
     except (torch.cuda.OutOfMemoryError, RuntimeError, MemoryError) as exc:
         if isinstance(exc, RuntimeError) and "memory" not in str(exc).lower():
             raise
@@ -192,6 +197,8 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
         else:
             t_d = torch.from_numpy(_times(sats, times)).to(dev.device)
         t_d = t_d.contiguous()
+        if t_d.data_ptr() % 16:              # the vector path wants 16-B aligned times
+            t_d = t_d.clone()
         m = int(t_d.shape[0])
         if out is None:
             planes, error = _alloc_grid(sats.n, m, dev.precision, dev.device)
@@ -278,7 +285,7 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
             rows, cols = tile
             tr, tc = rows.stop - rows.start, cols.stop - cols.start
             planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
-            _device.propagate_grid(dev, t_d[cols], planes_d, err_d,
+            _device.propagate_grid(dev, t_d[cols].clone(), planes_d, err_d,
                                    rows=(rows.start, rows.stop))
             planes_h, err_h = _alloc_grid(tr, tc, dev.precision, "cpu", pin=True)
             planes_h.copy_(planes_d, non_blocking=True)

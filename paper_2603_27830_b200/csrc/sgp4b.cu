@@ -6,8 +6,8 @@
 //   grid_kernel<T>     1 warp = 1 satellite x 128 time steps (4 per lane);
 //                      _propagate + solve_kepler + merge, kernel.py:325-534,
 //                      over the dense grid of propagate_batch, batch.py:166-205
-//   pairs_kernel<T>    1 thread / (satellite, time) pair; sgp4_propagate's
-//                      broadcasting form, kernel.py:513-534
+//   (pairs)            sgp4_propagate's broadcasting form (kernel.py:513-534)
+//                      runs through grid_kernel as P one-step rows
 //   kepler_kernel<T>   solve_kepler, kernel.py:325-349
 //
 // Numerics
@@ -31,6 +31,7 @@
 #include <float.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <math_constants.h>
 
 #include "../../include/sgp4b.h"
 
@@ -1142,44 +1143,6 @@ __device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kC
   }
 }
 
-// single cell with the same dispatch (pairs kernel): identical arithmetic
-// to the grid kernel's cells, so batch == scalar bit for bit
-template <bool ISIMP, int KITER, bool LO>
-__device__ __forceinline__ void one2(const Rec<float>& R, float th, float tl, const Grav& g,
-                                     float (&o)[6], int& code) {
-  VN<2> r[6];
-  int c2[2];
-  cellv<ISIMP, KITER, LO, 2>(R, sp<2>(th), sp<2>(tl), g, r, c2);
-#pragma unroll
-  for (int p = 0; p < 6; ++p) o[p] = r[p].h[0].x;
-  code = c2[0];
-}
-template <bool LO>
-__device__ __forceinline__ void compute_one(const Rec<float>& R, float th, float tl, const Grav& g,
-                                            float (&o)[6], int& code) {
-  const int flags = R.flags();
-  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
-  if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) one2<false, 1, LO>(R, th, tl, g, o, code);
-    else if (kit == 2) one2<false, 2, LO>(R, th, tl, g, o, code);
-    else if (kit == 3) one2<false, 3, LO>(R, th, tl, g, o, code);
-    else one2<false, 0, LO>(R, th, tl, g, o, code);
-  } else {
-    if (kit == 1) one2<true, 1, LO>(R, th, tl, g, o, code);
-    else if (kit == 2) one2<true, 2, LO>(R, th, tl, g, o, code);
-    else if (kit == 3) one2<true, 3, LO>(R, th, tl, g, o, code);
-    else one2<true, 0, LO>(R, th, tl, g, o, code);
-  }
-}
-template <bool LO>
-__device__ __forceinline__ void compute_one(const Rec<double>& R, double th, float, const Grav& g,
-                                            double (&o)[6], int& code) {
-  Cell64 c;
-  cell64(R, th, g, c);
-  o[0] = c.r[0]; o[1] = c.r[1]; o[2] = c.r[2];
-  o[3] = c.v[0]; o[4] = c.v[1]; o[5] = c.v[2];
-  code = c.code;
-}
 
 // One satellite row, chunks [c0, c1): per lane kCellsPerLane consecutive
 // steps per chunk.  CellsFn(th, tl, out, code) evaluates a lane's cells;
@@ -1195,8 +1158,8 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     if (j0 >= m) break;                     // only the row's last chunk is partial
     T th[kCellsPerLane];
     float tl[kCellsPerLane];
-    const bool full = j0 + kCellsPerLane <= m;
-    if (VEC && full) {
+    const bool full = VEC && j0 + kCellsPerLane <= m;
+    if (full) {
       ld_vec<kCellsPerLane>(times + j0, th);
     } else {
 #pragma unroll
@@ -1211,7 +1174,7 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
 
     T* base = row + j0;
     int32_t* cbase = crow + j0;
-    if (VEC && full) {
+    if (full) {
 #pragma unroll
       for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
       st_vec_cs<kCellsPerLane>(cbase, code);
@@ -1276,12 +1239,22 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
 #ifndef SGP4B_SMEM_REC
 #define SGP4B_SMEM_REC 0
 #endif
+
+//
+// The same kernel instance (VEC = true) also serves the scalar/broadcasting
+// API: with rec_idx set, row r uses record rec_idx[r] and times + r*times_ld,
+// so a list of (satellite, time) pairs runs as P rows of one step (never the
+// vector path) through exactly the instructions that compute an aligned
+// dense grid: batch == scalar bit for bit, whatever contraction choices the
+// compiler made.  The Python layer pads unaligned grids so every public call
+// runs this instance; VEC = false only serves raw C-ABI callers with
+// unaligned strides.
 template <typename T, bool VEC, bool LO>
 __global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 2)
-grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
-            const float* __restrict__ times_lo, int64_t m, Grav g, T* __restrict__ planes,
-            int64_t plane_stride, int64_t row_stride, int32_t* __restrict__ codes,
-            int64_t code_stride, int64_t chunks) {
+grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t n,
+            const T* __restrict__ times, const float* __restrict__ times_lo, int64_t times_ld,
+            int64_t m, Grav g, T* __restrict__ planes, int64_t plane_stride, int64_t row_stride,
+            int32_t* __restrict__ codes, int64_t code_stride, int64_t chunks) {
   const int64_t nwarps = (int64_t)gridDim.x * (kGridBlock / 32);
   const int64_t w = ((int64_t)blockIdx.x * kGridBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1300,40 +1273,19 @@ grid_kernel(const T* __restrict__ rec, int64_t n, const T* __restrict__ times,
     const int64_t sat = gi / chunks;
     const int64_t c0 = gi - sat * chunks;
     const int64_t c1 = (g1 - gi < chunks - c0) ? c0 + (g1 - gi) : chunks;
+    const int64_t ri = rec_idx != nullptr ? __ldg(rec_idx + sat) : sat;
 #if SGP4B_SMEM_REC
     __syncwarp();
-    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + sat * S_COUNT + i);
+    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + ri * S_COUNT + i);
     __syncwarp();
 #else
-    load_rec(rec + sat * S_COUNT, R);
+    load_rec(rec + ri * S_COUNT, R);
 #endif
-    dispatch_row<VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, planes + sat * row_stride,
-                          plane_stride, codes + sat * code_stride);
+    dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
+                     LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
+                     plane_stride, codes + sat * code_stride);
     gi += c1 - c0;
   }
-}
-
-// ======================================================================
-// Propagate: elementwise pairs (broadcasting sgp4_propagate)
-// ======================================================================
-template <typename T>
-__global__ void __launch_bounds__(256)
-pairs_kernel(const T* __restrict__ rec, const int64_t* __restrict__ idx, const T* __restrict__ times,
-             const float* __restrict__ times_lo, int64_t p, Grav g, T* __restrict__ rv,
-             int32_t* __restrict__ codes) {
-  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= p) return;
-  Rec<T> R;
-  load_rec(rec + idx[k] * S_COUNT, R);
-  T o[6];
-  int code;
-  if (times_lo != nullptr)
-    compute_one<true>(R, times[k], times_lo[k], g, o, code);
-  else
-    compute_one<false>(R, times[k], 0.0f, g, o, code);
-#pragma unroll
-  for (int q = 0; q < 6; ++q) rv[q * p + k] = o[q];
-  codes[k] = code;
 }
 
 template <typename T>
@@ -1342,6 +1294,30 @@ __global__ void kepler_kernel(const T* __restrict__ axnl, const T* __restrict__ 
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   out[k] = kepler_reference<T>(axnl[k], aynl[k], u[k]);
+}
+
+// |r32 - r64| and |v32 - v64| per cell in fp64 where both codes are 0,
+// +inf elsewhere (so a per-column sort puts excluded cells last).
+__global__ void drift_norms_kernel(const float* __restrict__ p32, const double* __restrict__ p64,
+                                   const int32_t* __restrict__ c32, const int32_t* __restrict__ c64,
+                                   int64_t cells, double* __restrict__ dr, double* __restrict__ dv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cells) return;
+  if (c32[i] != 0 || c64[i] != 0) {
+    dr[i] = CUDART_INF;
+    dv[i] = CUDART_INF;
+    return;
+  }
+  double r2 = 0.0, v2 = 0.0;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const double a = (double)__ldg(p32 + p * cells + i) - __ldg(p64 + p * cells + i);
+    const double b = (double)__ldg(p32 + (p + 3) * cells + i) - __ldg(p64 + (p + 3) * cells + i);
+    r2 = fma(a, a, r2);
+    v2 = fma(b, b, v2);
+  }
+  dr[i] = sqrt(r2);
+  dv[i] = sqrt(v2);
 }
 
 bool grav_from(const double* grav, Grav& g) {
@@ -1359,20 +1335,19 @@ bool grav_from(const double* grav, Grav& g) {
 
 // blocks of grid_kernel that fit on the current device at once (cached per
 // device and variant): the persistent grid size.
-int64_t resident_blocks(int precision, bool vec) {
-  static int cache[64][4];
+int64_t resident_blocks(int precision) {
+  static int cache[64][2];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
     fail(SGP4B_ECUDA, "cudaGetDevice failed");
     return -1;
   }
-  const int v = (precision == 64 ? 2 : 0) + (vec ? 1 : 0);
+  const int v = precision == 64 ? 1 : 0;
   if (cache[dev][v] > 0) return cache[dev][v];
   int sms = 0, per_sm = 0;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const void* fn = precision == 64
-      ? (vec ? (const void*)grid_kernel<double, true, false> : (const void*)grid_kernel<double, false, false>)
-      : (vec ? (const void*)grid_kernel<float, true, false> : (const void*)grid_kernel<float, false, false>);
+  const void* fn = precision == 64 ? (const void*)grid_kernel<double, true, false>
+                                    : (const void*)grid_kernel<float, true, false>;
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridBlock, 0);
   if (e != cudaSuccess || sms <= 0 || per_sm <= 0) {
     fail(SGP4B_ECUDA, "occupancy query: %s", cudaGetErrorString(e));
@@ -1380,6 +1355,35 @@ int64_t resident_blocks(int precision, bool vec) {
   }
   cache[dev][v] = sms * per_sm;
   return cache[dev][v];
+}
+
+// persistent launch of grid_kernel (dense grid or, with rec_idx, pairs)
+int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* times,
+                const float* times_lo, int64_t times_ld, int64_t m, int precision, const Grav& g,
+                void* planes, int64_t plane_stride, int64_t row_stride, int32_t* codes,
+                int64_t code_stride, bool vec, cudaStream_t s, const char* what) {
+  const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
+  const int64_t warps = n * chunks;
+  int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
+  const int64_t slots = resident_blocks(precision);
+  if (slots <= 0) return fail(SGP4B_ECUDA, "%s: %s", what, g_last_error);
+  if (blocks > slots) blocks = slots;
+  if (precision == 64) {
+    auto k = vec ? grid_kernel<double, true, false> : grid_kernel<double, false, false>;
+    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(
+        static_cast<const double*>(rec), rec_idx, n, static_cast<const double*>(times), nullptr,
+        times_ld, m, g, static_cast<double*>(planes), plane_stride, row_stride, codes,
+        code_stride, chunks);
+  } else {
+    auto k = times_lo != nullptr
+                 ? (vec ? grid_kernel<float, true, true> : grid_kernel<float, false, true>)
+                 : (vec ? grid_kernel<float, true, false> : grid_kernel<float, false, false>);
+    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(
+        static_cast<const float*>(rec), rec_idx, n, static_cast<const float*>(times), times_lo,
+        times_ld, m, g, static_cast<float*>(planes), plane_stride, row_stride, codes, code_stride,
+        chunks);
+  }
+  return check_launch(what);
 }
 
 inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
@@ -1404,7 +1408,9 @@ int sgp4b_init(const double* elements_dev, int64_t n, const double* grav, int pr
     return fail(SGP4B_EINVAL, "sgp4b_init: precision must be 32 or 64, got %d", precision);
   if (!elements_dev || !satrec_dev || !init_code_dev || !isimp_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_init: null pointer argument");
-  init_kernel<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+  // one warp per block: init is a long fp64 dependency chain per thread, so
+  // spread the few satellite-warps over as many SMs as possible
+  init_kernel<<<blocks_for(n, 32), 32, 0, (cudaStream_t)stream>>>(
       elements_dev, n, g, satrec_dev, init_code_dev, isimp_dev, record_dev, precision);
   return check_launch("sgp4b_init");
 }
@@ -1417,7 +1423,7 @@ int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev, const uin
     return fail(SGP4B_EINVAL, "sgp4b_pack: precision must be 32 or 64, got %d", precision);
   if (!satrec_dev || !init_code_dev || !isimp_dev || !record_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_pack: null pointer argument");
-  pack_kernel<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+  pack_kernel<<<blocks_for(n, 32), 32, 0, (cudaStream_t)stream>>>(
       satrec_dev, init_code_dev, isimp_dev, n, g, record_dev, precision);
   return check_launch("sgp4b_pack");
 }
@@ -1440,31 +1446,9 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_de
   const bool vec = (plane_stride % 4 == 0) && (row_stride % 4 == 0) && (code_stride % 4 == 0) &&
                    ((uintptr_t)planes_dev % (4 * esz) == 0) && ((uintptr_t)codes_dev % 16 == 0) &&
                    ((uintptr_t)times_dev % (4 * esz) == 0);
-  const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
-  const int64_t warps = n * chunks;
-  int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
-  const int64_t slots = resident_blocks(precision, vec);
-  if (slots <= 0) return fail(SGP4B_ECUDA, "sgp4b_propagate_grid: %s", g_last_error);
-  if (blocks > slots) blocks = slots;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (precision == 64) {
-    const double* rec = static_cast<const double*>(record_dev);
-    const double* t = static_cast<const double*>(times_dev);
-    double* out = static_cast<double*>(planes_dev);
-    auto k = vec ? grid_kernel<double, true, false> : grid_kernel<double, false, false>;
-    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(rec, n, t, nullptr, m, g, out, plane_stride,
-                                              row_stride, codes_dev, code_stride, chunks);
-  } else {
-    const float* rec = static_cast<const float*>(record_dev);
-    const float* t = static_cast<const float*>(times_dev);
-    float* out = static_cast<float*>(planes_dev);
-    const bool lo = times_lo_dev != nullptr;
-    auto k = vec ? (lo ? grid_kernel<float, true, true> : grid_kernel<float, true, false>)
-                 : (lo ? grid_kernel<float, false, true> : grid_kernel<float, false, false>);
-    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(rec, n, t, times_lo_dev, m, g, out, plane_stride,
-                                              row_stride, codes_dev, code_stride, chunks);
-  }
-  return check_launch("sgp4b_propagate_grid");
+  return launch_grid(record_dev, nullptr, n, times_dev, times_lo_dev, 0, m, precision, g,
+                     planes_dev, plane_stride, row_stride, codes_dev, code_stride, vec,
+                     (cudaStream_t)stream, "sgp4b_propagate_grid");
 }
 
 int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, const void* times_dev,
@@ -1476,16 +1460,24 @@ int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, co
     return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: precision must be 32 or 64, got %d", precision);
   if (!record_dev || !sat_idx_dev || !times_dev || !rv_dev || !codes_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: null pointer argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (precision == 64)
-    pairs_kernel<double><<<blocks_for(p, 256), 256, 0, s>>>(
-        static_cast<const double*>(record_dev), sat_idx_dev, static_cast<const double*>(times_dev),
-        nullptr, p, g, static_cast<double*>(rv_dev), codes_dev);
-  else
-    pairs_kernel<float><<<blocks_for(p, 256), 256, 0, s>>>(
-        static_cast<const float*>(record_dev), sat_idx_dev, static_cast<const float*>(times_dev),
-        times_lo_dev, p, g, static_cast<float*>(rv_dev), codes_dev);
-  return check_launch("sgp4b_propagate_pairs");
+  // P rows of one step: row k = record sat_idx[k] at times[k]; output (6, P).
+  // The VEC instance (m = 1 never takes its vector path) is the one aligned
+  // grids use, so a pair equals the corresponding grid cell bit for bit.
+  return launch_grid(record_dev, sat_idx_dev, p, times_dev, times_lo_dev, 1, 1, precision, g,
+                     rv_dev, p, 1, codes_dev, 1, true, (cudaStream_t)stream,
+                     "sgp4b_propagate_pairs");
+}
+
+int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
+                      const int32_t* codes32_dev, const int32_t* codes64_dev, int64_t n, int64_t m,
+                      double* dr_dev, double* dv_dev, void* stream) {
+  if (n <= 0 || m <= 0) return fail(SGP4B_EINVAL, "sgp4b_drift_norms: empty grid");
+  if (!planes32_dev || !planes64_dev || !codes32_dev || !codes64_dev || !dr_dev || !dv_dev)
+    return fail(SGP4B_EINVAL, "sgp4b_drift_norms: null pointer argument");
+  const int64_t cells = n * m;
+  drift_norms_kernel<<<blocks_for(cells, 256), 256, 0, (cudaStream_t)stream>>>(
+      planes32_dev, planes64_dev, codes32_dev, codes64_dev, cells, dr_dev, dv_dev);
+  return check_launch("sgp4b_drift_norms");
 }
 
 int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev, const void* u_dev, int64_t n,

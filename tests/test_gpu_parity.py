@@ -172,10 +172,10 @@ def test_row_shards_bitwise_equal_full_grid(corpus_columns, precision):
     sats = pkg.init_batch(corpus_columns[:, :301], precision=precision)
     times = np.linspace(0.0, 1440.0, 77)
     full = pkg.propagate_batch_device(sats, times)
+    from paper_2603_27830_b200.batch import _alloc_grid
     t_d = torch.from_numpy(times.astype(sats.dtype)).cuda()
     for lo, hi in pkg.partition_work(301, 1, 4):
-        planes = torch.empty((6, hi - lo, 77), dtype=full.planes.dtype, device="cuda")
-        err = torch.empty((hi - lo, 77), dtype=torch.int32, device="cuda")
+        planes, err = _alloc_grid(hi - lo, 77, precision, torch.device("cuda"))
         _device.propagate_grid(sats.device_satrec, t_d, planes, err, rows=(lo, hi))
         assert torch.equal(planes, full.planes[:, lo:hi])
         assert torch.equal(err, full.error[lo:hi])
@@ -291,3 +291,70 @@ def test_starlink_full_size_properties():
     assert (ref_c == 0).all()
     assert np.abs(got[:3].T - ref_r).max() <= TOL64_R
     assert np.abs(got[3:].T - ref_v).max() <= TOL64_V
+
+
+def test_drift_report_gpu(corpus_columns):
+    """drift_report on the GPU: the reference's acceptance bands
+    (test_acceptance.py:107-122) and nearest-rank percentiles identical to a
+    host recomputation from the same two device grids."""
+    import dataclasses as dc
+    import math as _m
+    pkg = _gpu()
+    from paper_2603_27830_b200.tle import MeanElements
+    els = [MeanElements(*corpus_columns[:, i], 2023, 1, 0.0) for i in range(120)]
+    rep = pkg.drift_report(els, horizon_days=14.0, step_minutes=90.0)
+    epoch_m = rep.p50_km[0] * 1000.0
+    print(f"\ndrift: epoch median {epoch_m:.3f} m, day-14 median {rep.p50_km[-1]:.4f} km, "
+          f"{rep.p50_kms[-1] * 1000:.4f} m/s")
+    assert 0.1 <= epoch_m <= 10.0
+    assert rep.p50_km[-1] < 1.0 and rep.p50_kms[-1] * 1000.0 < 10.0
+    # host recomputation with the reference's nearest-rank rule
+    times = np.arange(0.0, 14.0 * 1440.0 + 45.0, 90.0)
+    lo = pkg.propagate_batch(pkg.init_batch(els, precision=32), times)
+    hi = pkg.propagate_batch(pkg.init_batch(els, precision=64), times)
+    inc = (lo.error == 0) & (hi.error == 0)
+    dr = np.linalg.norm(lo.r.astype(np.float64) - hi.r, axis=-1)
+    for j in (0, 37, len(times) - 1):
+        v = np.sort(dr[inc[:, j], j])
+        want = v[max(1, int(np.ceil(0.5 * v.size))) - 1]
+        assert rep.p50_km[j] == want
+    assert rep.included_cells == int(inc.sum())
+    csv_text = pkg.emit_report_csv(rep)
+    assert csv_text.splitlines()[0].startswith("day,p5_km")
+    bad = [dc.replace(els[0], no_kozai=0.0)]
+    with pytest.raises(pkg.EmptyReportError):
+        pkg.drift_report(bad, 1.0, 60.0)
+    assert not _m.isnan(rep.p95_kms[-1])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_randomized_grids(oracle, corpus_columns, seed):
+    """Random sub-catalogues and time grids (incl. negative and 14-day
+    times): fp64 within tolerance, codes equal at both precisions, and the
+    broadcasting scalar API equal to the batch bit for bit."""
+    pkg = _gpu()
+    rng = np.random.default_rng(seed)
+    n, m = int(rng.integers(1, 40)), int(rng.integers(1, 300))
+    cols = corpus_columns[:, rng.integers(0, corpus_columns.shape[1], n)]
+    times = np.sort(rng.uniform(-1440.0, 20160.0, m))
+    ref64, codes64 = oracle.grid(oracle.init_columns(cols, 64), times)
+    _, codes32 = oracle.grid(oracle.init_columns(cols, 32), times)
+    for precision, dtype, ref_codes in ((64, np.float64, codes64), (32, np.float32, codes32)):
+        sats = pkg.init_batch(cols, precision=precision)
+        res = pkg.propagate_batch(sats, times)
+        assert np.array_equal(res.error, ref_codes)
+        assert np.array_equal(res.error, codes64)
+        if precision == 64:
+            dr, dv = _diff(res.planes, ref64, ref_codes == 0)
+            assert dr.max(initial=0) <= TOL64_R and dv.max(initial=0) <= TOL64_V
+        # broadcasting scalar API: the batch's own SatInit (n,) against
+        # times (m, 1) -> (m, n).  (A hand-edited fp32 SatInit would be
+        # re-packed from its fp32-rounded fields, like the reference's fp32
+        # path, so it is not expected to match the fp64-initialised batch.)
+        st = pkg.sgp4_propagate(sats.init, times.astype(dtype)[:, None])
+        assert st.r.shape == (m, n, 3)
+        # error cells may carry NaN (as in the reference), hence equal_nan
+        assert np.array_equal(np.transpose(st.r, (2, 1, 0)), res.planes[:3], equal_nan=True)
+        assert np.array_equal(np.transpose(st.v, (2, 1, 0)), res.planes[3:], equal_nan=True)
+        st = type(st)(r=st.r, v=st.v, error_code=st.error_code.T)
+        assert np.array_equal(st.error_code, res.error)
