@@ -660,6 +660,16 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     tq = esine * fma2(x, fma2(x, fma2(x, 0.0390625f, 0.0625f), 0.125f), 0.5f);
     rvdotl = sqam * betal * irl;                           // sqrt(am (1-x)) / rl
     ipl = (rsam * rsam) * fma2(x, fma2(x, x + 1.0f, 1.0f), 1.0f);
+  } else if constexpr (KITER == 1 || KITER == 2) {
+    // e < 0.1: pl = am (1 - el2) > 0, so 1/sqrt(pl) = rsqrt(am) / betal and
+    // one SFU rsqrt serves betal, sqrt(pl) and 1/pl
+    const V2 omel2 = 1.0f - el2;
+    const V2 rb = rsq2(omel2);
+    betal = omel2 * rb;
+    rvdotl = sqam * betal * irl;                           // sqrt(pl) / rl
+    tq = esine * rcp2(betal + 1.0f);
+    const V2 rspl = rsam * rb;
+    ipl = rspl * rspl;
   } else {
     const V2 rspl = rsq2(pl_safe);
     rvdotl = (pl_safe * rspl) * irl;                       // sqrt(pl) / rl
