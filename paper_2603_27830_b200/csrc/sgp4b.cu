@@ -32,8 +32,25 @@
 #include <stdio.h>
 #include <stdarg.h>
 #include <math_constants.h>
+#include <type_traits>
 
 #include "../../include/sgp4b.h"
+
+// build-time tuning knobs (defaults are the shipped configuration)
+#ifndef SGP4B_SMEM_REC
+#define SGP4B_SMEM_REC 0          // fp32 records in shared memory (default: registers)
+#endif
+#ifndef SGP4B_SMEM_REC64
+#define SGP4B_SMEM_REC64 1        // fp64 records (80 registers) in shared memory
+#endif
+#ifndef SGP4B_F64_UNROLL
+#define SGP4B_F64_UNROLL 1
+#endif
+constexpr int kF64Unroll = SGP4B_F64_UNROLL;   // fp64 cells interleaved per lane
+#ifndef SGP4B_MINB64
+#define SGP4B_MINB64 3
+#endif
+constexpr int kGridMinBlocks64 = SGP4B_MINB64; // resident 256-thread blocks per SM (fp64)
 
 namespace {
 
@@ -264,7 +281,8 @@ __device__ __forceinline__ void rotate64(double s, double c, double d, double x,
 // corrections of su and xinc are applied as rotations (rotate64), and the
 // atan2 of kernel.py:455 is replaced by normalising (sin u, cos u) — only
 // sin/cos of su are ever used.  All of it is exact to fp64 rounding.
-__device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Grav& g, Cell64& o) {
+template <class RT>
+__device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cell64& o) {
   const double tiny = DBL_MIN;
   const double xke = g.xke, j2 = g.j2, re = g.re;
   const double vkmpersec = g.vkm;
@@ -272,50 +290,50 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   const bool isimp = flags & FLAG_ISIMP;
 
   // secular gravity and atmospheric drag  kernel.py:365-391
-  const double xmdf = R.v[S_MO] + R.v[S_MDOT] * t;
-  const double argpdf = R.v[S_ARGPO] + R.v[S_ARGPDOT] * t;
-  const double nodedf = R.v[S_NODEO] + R.v[S_NODEDOT] * t;
+  const double xmdf = R[S_MO] + R[S_MDOT] * t;
+  const double argpdf = R[S_ARGPO] + R[S_ARGPDOT] * t;
+  const double nodedf = R[S_NODEO] + R[S_NODEDOT] * t;
   const double t2 = t * t;
-  double nodem = nodedf + R.v[S_NODECF] * t2;
-  double tempa = 1.0 - R.v[S_CC1] * t;
-  double tempe = R.v[S_BC4] * t;
-  double templ = R.v[S_T2COF] * t2;
+  double nodem = nodedf + R[S_NODECF] * t2;
+  double tempa = 1.0 - R[S_CC1] * t;
+  double tempe = R[S_BC4] * t;
+  double templ = R[S_T2COF] * t2;
   double mm = xmdf, argpm = argpdf;
   if (!isimp) {
     double sx, cx;
     sincos(xmdf, &sx, &cx);
-    const double delomg = R.v[S_OMGCOF] * t;
-    const double delmtemp = 1.0 + R.v[S_ETA] * cx;
-    const double delm = R.v[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R.v[S_DELMO]);
+    const double delomg = R[S_OMGCOF] * t;
+    const double delmtemp = 1.0 + R[S_ETA] * cx;
+    const double delm = R[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R[S_DELMO]);
     const double temp = delomg + delm;
     mm = xmdf + temp;
     argpm = argpdf - temp;
     const double t3 = t2 * t;
     const double t4 = t3 * t;
-    tempa = tempa - R.v[S_D2] * t2 - R.v[S_D3] * t3 - R.v[S_D4] * t4;
+    tempa = tempa - R[S_D2] * t2 - R[S_D3] * t3 - R[S_D4] * t4;
     double smm, cmm;
     rotate64(sx, cx, temp, mm, smm, cmm);                // sin(mm)
-    tempe = tempe + R.v[S_BC5] * (smm - R.v[S_SINMAO]);
-    templ = templ + R.v[S_T3COF] * t3 + t4 * (R.v[S_T4COF] + t * R.v[S_T5COF]);
+    tempe = tempe + R[S_BC5] * (smm - R[S_SINMAO]);
+    templ = templ + R[S_T3COF] * t3 + t4 * (R[S_T4COF] + t * R[S_T5COF]);
   }
 
   // mean motion / eccentricity update  kernel.py:393-414
-  const double am = R.v[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
+  const double am = R[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
   const double am_safe = gmax(am, tiny);
   const double sqam = sqrt(am_safe);
   const double nm = xke / (am_safe * sqam);       // xke / am^1.5
-  double em = R.v[S_ECCO] - tempe;
+  double em = R[S_ECCO] - tempe;
   const bool bad_em = (em >= 1.0) || (em < -0.001);
   em = em < 1.0e-6 ? 1.0e-6 : em;
-  mm = mm + R.v[S_NO] * templ;
+  mm = mm + R[S_NO] * templ;
   double xlm = mm + argpm + nodem;
   nodem = fmod_2pi(nodem);              // mod_twopi_signed, dmath.py:218-221
   argpm = pymod_2pi(argpm);
   xlm = pymod_2pi(xlm);
   mm = pymod_2pi(xlm - argpm - nodem);
 
-  const double sinip = R.v[S_SINIO];
-  const double cosip = R.v[S_COSIO];
+  const double sinip = R[S_SINIO];
+  const double cosip = R[S_COSIO];
 
   // long-period periodics  kernel.py:419-431
   const double ep = em;
@@ -324,8 +342,8 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   const double axnl = ep * ca;
   const double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
   const double ilp = 1.0 / pl_lp;
-  const double aynl = ep * sa + ilp * R.v[S_AYCOF];
-  const double xl = mm + argpm + nodem + ilp * R.v[S_XLCOF] * axnl;
+  const double aynl = ep * sa + ilp * R[S_AYCOF];
+  const double xl = mm + argpm + nodem + ilp * R[S_XLCOF] * axnl;
 
   // Kepler  kernel.py:325-349, 434-437: (sin, cos) of E carried along the
   // Newton updates by rotation
@@ -370,9 +388,9 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   const double temp2 = temp1 * ipl;
 
   // short-period periodics  kernel.py:463-469
-  const double con41 = R.v[S_CON41], x1mth2 = R.v[S_X1MTH2];
+  const double con41 = R[S_CON41], x1mth2 = R[S_X1MTH2];
   const double mrt = rl * (1.0 - 1.5 * temp2 * betal * con41) + 0.5 * temp1 * x1mth2 * cos2u;
-  const double dsu = -0.25 * temp2 * R.v[S_X7THM1] * sin2u;
+  const double dsu = -0.25 * temp2 * R[S_X7THM1] * sin2u;
   const double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
   const double dinc = 1.5 * temp2 * cosip * sinip * cos2u;
   const double nmx = nm * temp1 / xke;
@@ -386,7 +404,7 @@ __device__ __forceinline__ void cell64(const Rec<double>& R, double t, const Gra
   else
     sincos(atan2(sinu, cosu) + dsu, &sinsu, &cossu);
   sincos(xnode, &snod, &cnod);
-  rotate64(sinip, cosip, dinc, R.v[S_INCLO] + dinc, sini, cosi);
+  rotate64(sinip, cosip, dinc, R[S_INCLO] + dinc, sini, cosi);
   const double xmx = -snod * cosi;
   const double xmy = cnod * cosi;
   const double mr = mrt * re;
@@ -1138,15 +1156,11 @@ __device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kC
                                               const float (&)[kCellsPerLane], const Grav& g,
                                               double (&out)[6][kCellsPerLane],
                                               int (&code)[kCellsPerLane]) {
-  Rec<double> RR;
-#pragma unroll
-  for (int i = 0; i < S_COUNT; ++i) RR.v[i] = R[i];
-  // one fp64 cell at a time: the fp64 pipe, not issue, is the limit, and
-  // keeping registers low doubles the resident warps
-#pragma unroll 1
+  // fp64 cells are FP64-latency bound: SGP4B_F64_UNROLL cells interleave
+#pragma unroll kF64Unroll
   for (int k = 0; k < kCellsPerLane; ++k) {
     Cell64 c;
-    cell64(RR, th[k], g, c);
+    cell64(R, th[k], g, c);
     out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
     out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
     code[k] = c.code;
@@ -1246,9 +1260,7 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
 // Persistent warps: the (satellite, chunk) work items of the grid are split
 // into one contiguous range per resident warp; the warp walks it row by row,
 // loading each satellite's record once and dispatching its class once.
-#ifndef SGP4B_SMEM_REC
-#define SGP4B_SMEM_REC 0
-#endif
+
 
 //
 // The same kernel instance (VEC = true) also serves the scalar/broadcasting
@@ -1260,7 +1272,7 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
 // runs this instance; VEC = false only serves raw C-ABI callers with
 // unaligned strides.
 template <typename T, bool VEC, bool LO>
-__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : 2)
+__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : kGridMinBlocks64)
 grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t n,
             const T* __restrict__ times, const float* __restrict__ times_lo, int64_t times_ld,
             int64_t m, Grav g, T* __restrict__ planes, int64_t plane_stride, int64_t row_stride,
@@ -1272,25 +1284,24 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
   const int64_t g0 = total * w / nwarps;
   const int64_t g1 = total * (w + 1) / nwarps;
 
-#if SGP4B_SMEM_REC
-  __shared__ __align__(16) T srec[kGridBlock / 32][S_COUNT];
-  T* my = srec[threadIdx.x >> 5];
-  RecS<T> R{my};
-#else
-  Rec<T> R;
-#endif
+  constexpr bool kSmem = sizeof(T) == 8 ? SGP4B_SMEM_REC64 : SGP4B_SMEM_REC;
+  __shared__ __align__(16) T srec[kSmem ? kGridBlock / 32 : 1][S_COUNT];
+  T* my = srec[kSmem ? (threadIdx.x >> 5) : 0];
+  using RecT = typename std::conditional<kSmem, RecS<T>, Rec<T>>::type;
+  RecT R;
+  if constexpr (kSmem) R.p = my;
   for (int64_t gi = g0; gi < g1;) {
     const int64_t sat = gi / chunks;
     const int64_t c0 = gi - sat * chunks;
     const int64_t c1 = (g1 - gi < chunks - c0) ? c0 + (g1 - gi) : chunks;
     const int64_t ri = rec_idx != nullptr ? __ldg(rec_idx + sat) : sat;
-#if SGP4B_SMEM_REC
-    __syncwarp();
-    for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + ri * S_COUNT + i);
-    __syncwarp();
-#else
-    load_rec(rec + ri * S_COUNT, R);
-#endif
+    if constexpr (kSmem) {
+      __syncwarp();
+      for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + ri * S_COUNT + i);
+      __syncwarp();
+    } else {
+      load_rec(rec + ri * S_COUNT, R);
+    }
     dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
                      LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
                      plane_stride, codes + sat * code_stride);
