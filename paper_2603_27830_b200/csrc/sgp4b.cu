@@ -48,7 +48,7 @@
 #endif
 constexpr int kF64Unroll = SGP4B_F64_UNROLL;   // fp64 cells interleaved per lane
 #ifndef SGP4B_MINB64
-#define SGP4B_MINB64 3
+#define SGP4B_MINB64 2
 #endif
 constexpr int kGridMinBlocks64 = SGP4B_MINB64; // resident 256-thread blocks per SM (fp64)
 
@@ -70,6 +70,7 @@ struct Grav {
   double mu, re, xke, tumin, j2, j3, j4, j3oj2;
   // derived on the host once per launch (propagate kernels)
   double vkm;                                    // re * xke / 60
+  double inv_xke;
   float xke_f, re_f, vkm_f, inv_xke_f, half_j2_f;
 };
 
@@ -259,6 +260,76 @@ struct Cell64 {
   int code;
 };
 
+// ---- lean fp64 primitives for the propagate cell ------------------------
+// The propagate cell's arguments are finite, normal and moderate (|x| well
+// below 2^20 pi/2 for sin/cos), so the special-case and slow paths of the
+// libdevice routines are dead weight; and libdevice materialises its 64-bit
+// polynomial constants with UMOV pairs on every call.  These versions keep
+// the coefficients in __constant__ memory (DFMA reads them directly) and
+// are accurate to ~1 ulp, far inside the 1 mm / 1e-6 km/s budget.
+__constant__ double c_sin_poly[6] = {
+    -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+    2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10};
+__constant__ double c_cos_poly[6] = {
+    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11};
+// pi/2 in three parts (33 + 33 + 53 bits) and 2/pi
+__constant__ double c_pio2[4] = {1.57079632673412561417e+00, 6.07710050630396597660e-11,
+                                 2.02226624879595063154e-21, 6.36619772367581382433e-01};
+
+__device__ __forceinline__ void sincos64(double x, double* sp, double* cp) {
+  const double k = rint(x * c_pio2[3]);
+  double r = fma(-k, c_pio2[0], x);           // exact: 33-bit part, |k| < 2^20
+  r = fma(-k, c_pio2[1], r);
+  r = fma(-k, c_pio2[2], r);
+  const double z = r * r;
+  const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, c_sin_poly[5], c_sin_poly[4]),
+                                                 c_sin_poly[3]), c_sin_poly[2]), c_sin_poly[1]),
+                        c_sin_poly[0]);
+  const double sr = fma(r * z, ps, r);
+  const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, c_cos_poly[5], c_cos_poly[4]),
+                                                 c_cos_poly[3]), c_cos_poly[2]), c_cos_poly[1]),
+                        c_cos_poly[0]);
+  const double cr = fma(z * z, pc, fma(-0.5, z, 1.0));
+  const int q = (int)k & 3;
+  const double s0 = (q & 1) ? cr : sr;
+  const double c0 = (q & 1) ? sr : cr;
+  *sp = (q & 2) ? -s0 : s0;
+  *cp = ((q + 1) & 2) ? -c0 : c0;
+}
+
+// 1/x and a/b: SFU seed + two Newton steps + one residual correction
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double div64(double a, double b) {
+  const double r = rcp64(b);
+  const double q = a * r;
+  return fma(r, fma(-b, q, a), q);
+}
+// sqrt(x) and 1/sqrt(x) for x > 0: SFU rsqrt seed + Newton, then a
+// Tuckerman-style correction of x * (1/sqrt x)
+__device__ __forceinline__ double rsqrt64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+__device__ __forceinline__ double sqrt64(double x) {
+  const double y = rsqrt64(x);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 // (sin, cos)(a + d) from (sin, cos)(a): series to d^7 / d^6 when
 // |d| < 2^-6 (truncation < 1e-19, below fp64 resolution of the result),
 // otherwise a direct sincos of the new angle `x`.
@@ -271,7 +342,7 @@ __device__ __forceinline__ void rotate64(double s, double c, double d, double x,
     so = fma(s, cd, c * sd);
     co = fma(c, cd, -s * sd);
   } else {
-    sincos(x, &so, &co);
+    sincos64(x, &so, &co);
   }
 }
 
@@ -301,7 +372,7 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   double mm = xmdf, argpm = argpdf;
   if (!isimp) {
     double sx, cx;
-    sincos(xmdf, &sx, &cx);
+    sincos64(xmdf, &sx, &cx);
     const double delomg = R[S_OMGCOF] * t;
     const double delmtemp = 1.0 + R[S_ETA] * cx;
     const double delm = R[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R[S_DELMO]);
@@ -320,8 +391,8 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   // mean motion / eccentricity update  kernel.py:393-414
   const double am = R[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
   const double am_safe = gmax(am, tiny);
-  const double sqam = sqrt(am_safe);
-  const double nm = xke / (am_safe * sqam);       // xke / am^1.5
+  const double sqam = sqrt64(am_safe);
+  const double nm = div64(xke, am_safe * sqam);   // xke / am^1.5
   double em = R[S_ECCO] - tempe;
   const bool bad_em = (em >= 1.0) || (em < -0.001);
   em = em < 1.0e-6 ? 1.0e-6 : em;
@@ -338,10 +409,10 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   // long-period periodics  kernel.py:419-431
   const double ep = em;
   double sa, ca;
-  sincos(argpm, &sa, &ca);
+  sincos64(argpm, &sa, &ca);
   const double axnl = ep * ca;
   const double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
-  const double ilp = 1.0 / pl_lp;
+  const double ilp = rcp64(pl_lp);
   const double aynl = ep * sa + ilp * R[S_AYCOF];
   const double xl = mm + argpm + nodem + ilp * R[S_XLCOF] * axnl;
 
@@ -349,12 +420,12 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   // Newton updates by rotation
   const double u = pymod_2pi(xl - nodem);
   double eo1 = u, sineo1, coseo1;
-  sincos(u, &sineo1, &coseo1);
+  sincos64(u, &sineo1, &coseo1);
   bool active = true;
 #pragma unroll 1
   for (int it = 0; it < 10 && active; ++it) {
     const double den = 1.0 - coseo1 * axnl - sineo1 * aynl;
-    double tem5 = (u - aynl * coseo1 + axnl * sineo1 - eo1) / den;
+    double tem5 = div64(u - aynl * coseo1 + axnl * sineo1 - eo1, den);
     tem5 = tem5 >= 0.95 ? 0.95 : (tem5 <= -0.95 ? -0.95 : tem5);
     eo1 = eo1 + tem5;
     rotate64(sineo1, coseo1, tem5, eo1, sineo1, coseo1);
@@ -370,20 +441,20 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   const double pl_safe = gmax(pl, tiny);
   const double rl = am_safe * (1.0 - ecose);
   const double rl_safe = rl == 0.0 ? tiny : rl;
-  const double irl = 1.0 / rl_safe;
+  const double irl = rcp64(rl_safe);
   const double rdotl = sqam * esine * irl;
-  const double rvdotl = sqrt(pl_safe) * irl;
-  const double betal = sqrt(gmax(1.0 - el2, tiny));
-  const double tq = esine / (1.0 + betal);
+  const double rvdotl = sqrt64(pl_safe) * irl;
+  const double betal = sqrt64(gmax(1.0 - el2, tiny));
+  const double tq = div64(esine, 1.0 + betal);
   // (sin u, cos u) normalised: the reference's am/rl factor is positive and
   // only the direction reaches sin/cos(su)
   const double sn = sineo1 - aynl - axnl * tq;
   const double cs = coseo1 - axnl + aynl * tq;
-  const double inrm = rsqrt(sn * sn + cs * cs);
+  const double inrm = rsqrt64(sn * sn + cs * cs);
   const double sinu = sn * inrm, cosu = cs * inrm;
   const double sin2u = (cosu + cosu) * sinu;
   const double cos2u = 1.0 - 2.0 * sinu * sinu;
-  const double ipl = 1.0 / pl_safe;
+  const double ipl = rcp64(pl_safe);
   const double temp1 = 0.5 * j2 * ipl;
   const double temp2 = temp1 * ipl;
 
@@ -393,7 +464,7 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   const double dsu = -0.25 * temp2 * R[S_X7THM1] * sin2u;
   const double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
   const double dinc = 1.5 * temp2 * cosip * sinip * cos2u;
-  const double nmx = nm * temp1 / xke;
+  const double nmx = nm * temp1 * g.inv_xke;
   const double mvt = rdotl - nmx * x1mth2 * sin2u;
   const double rvdot = rvdotl + nmx * (x1mth2 * cos2u + 1.5 * con41);
 
@@ -402,8 +473,8 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   if (fabs(dsu) < 0.015625)
     rotate64(sinu, cosu, dsu, 0.0, sinsu, cossu);
   else
-    sincos(atan2(sinu, cosu) + dsu, &sinsu, &cossu);
-  sincos(xnode, &snod, &cnod);
+    sincos64(atan2(sinu, cosu) + dsu, &sinsu, &cossu);
+  sincos64(xnode, &snod, &cnod);
   rotate64(sinip, cosip, dinc, R[S_INCLO] + dinc, sini, cosi);
   const double xmx = -snod * cosi;
   const double xmy = cnod * cosi;
@@ -1346,6 +1417,7 @@ bool grav_from(const double* grav, Grav& g) {
   g.mu = grav[0]; g.re = grav[1]; g.xke = grav[2]; g.tumin = grav[3];
   g.j2 = grav[4]; g.j3 = grav[5]; g.j4 = grav[6]; g.j3oj2 = grav[7];
   g.vkm = g.re * g.xke / 60.0;
+  g.inv_xke = 1.0 / g.xke;
   g.xke_f = (float)g.xke;
   g.re_f = (float)g.re;
   g.vkm_f = (float)g.vkm;
