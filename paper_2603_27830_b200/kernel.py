@@ -2,16 +2,18 @@
 
 ``sgp4_init`` and ``sgp4_propagate`` keep the reference's signatures,
 dataclasses and broadcasting rules, but both run on the GPU through
-libsgp4b.so: init is the fp64 init kernel, propagate is the pairs kernel,
-which evaluates exactly the same cell function as the dense-grid kernel
-behind ``propagate_batch`` — so a batch cell equals the scalar call at the
-same precision bit for bit (the reference's batch≡scalar contract,
-tests/test_batch.py:39-64).
+libsgp4b.so: init is the fp64 init kernel; propagate runs the same grid-
+kernel instance as ``propagate_batch`` — as one dense grid when the
+broadcast is a Cartesian product (satellite axes x time axes, e.g. init
+(n, 1) against times (m,)), otherwise as one-step rows of (satellite, time)
+pairs — so a batch cell equals the scalar call at the same precision bit for
+bit (the reference's batch≡scalar contract, tests/test_batch.py:39-64).
 """
 
 from __future__ import annotations
 
 import enum
+import dataclasses
 from dataclasses import dataclass, fields as dataclass_fields
 from typing import Any
 
@@ -181,10 +183,36 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
     v = np.empty(out_shape + (3,), dtype=dtype)
     if p == 0:
         return StateVector(r=r, v=v, error_code=np.zeros(out_shape, dtype=np.int32))
-    idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape), out_shape).ravel()
-    tt = np.ascontiguousarray(np.broadcast_to(t, out_shape).ravel())
     device = dev.device
+    nd = len(out_shape)
+    sat_p = (1,) * (nd - len(sat_shape)) + tuple(sat_shape)
+    t_p = (1,) * (nd - t.ndim) + tuple(t.shape)
+    sat_axes = [k for k in range(nd) if sat_p[k] > 1]
+    t_axes = [k for k in range(nd) if t_p[k] > 1]
     with torch.cuda.device(device):
+        if not set(sat_axes) & set(t_axes):
+            # Cartesian product (e.g. init (n, 1) x times (m,)): one dense grid
+            perm = sat_axes + t_axes + [k for k in range(nd) if k not in sat_axes + t_axes]
+            n_sel = int(np.prod([out_shape[k] for k in sat_axes], dtype=np.int64))
+            m_sel = int(np.prod([out_shape[k] for k in t_axes], dtype=np.int64))
+            sats = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape), out_shape)
+            rows = np.ascontiguousarray(sats.transpose(perm).reshape(n_sel, m_sel, -1)[:, 0, 0])
+            tsel = np.ascontiguousarray(
+                np.broadcast_to(t, out_shape).transpose(perm).reshape(n_sel, m_sel, -1)[0, :, 0])
+            grid = _grid_of_rows(dev, rows, tsel)
+            planes = grid[0].cpu().numpy()
+            codes = grid[1].cpu().numpy()
+            shape_p = tuple(out_shape[k] for k in perm)
+            inv = np.argsort(perm)
+            for dst, lo in ((r, 0), (v, 3)):
+                blk = planes[lo:lo + 3].reshape((3,) + shape_p)
+                dst[...] = np.moveaxis(blk.transpose([0] + [1 + a for a in inv]), 0, -1)
+            return StateVector(r=r, v=v,
+                               error_code=codes.reshape(shape_p).transpose(inv).copy())
+        # general broadcast: one (satellite, time) pair per cell
+        idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape),
+                              out_shape).ravel()
+        tt = np.ascontiguousarray(np.broadcast_to(t, out_shape).ravel())
         idx_d = torch.from_numpy(np.ascontiguousarray(idx)).to(device)
         t_d = torch.from_numpy(tt).to(device)
         rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
@@ -195,6 +223,21 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
     r[...] = rv_h[:3].T.reshape(out_shape + (3,))
     v[...] = rv_h[3:].T.reshape(out_shape + (3,))
     return StateVector(r=r, v=v, error_code=codes_h.reshape(out_shape))
+
+
+def _grid_of_rows(dev, rows: np.ndarray, times: np.ndarray):
+    """Dense grid for the satellites ``rows`` (indices into ``dev``) at
+    ``times``, through the same padded grid-kernel instance as
+    ``propagate_batch`` (so results equal the batch bit for bit)."""
+    from .batch import _alloc_grid
+    device = dev.device
+    rows_d = torch.from_numpy(rows).to(device)
+    sub = dataclasses.replace(dev, record=dev.record.index_select(0, rows_d).contiguous(),
+                              codes=dev.codes.index_select(0, rows_d))
+    t_d = torch.from_numpy(times).to(device)
+    planes, codes = _alloc_grid(int(rows.size), int(times.size), dev.precision, device)
+    _device.propagate_grid(sub, t_d, planes, codes)
+    return planes, codes
 
 
 def solve_kepler(axnl, aynl, u_init):

@@ -358,3 +358,11 @@ def test_randomized_grids(oracle, corpus_columns, seed):
         assert np.array_equal(np.transpose(st.v, (2, 1, 0)), res.planes[3:], equal_nan=True)
         st = type(st)(r=st.r, v=st.v, error_code=st.error_code.T)
         assert np.array_equal(st.error_code, res.error)
+        # general (non-Cartesian) broadcast: satellite i at its own time
+        jj = rng.integers(0, m, n)
+        sd = pkg.sgp4_propagate(sats.init, times.astype(dtype)[jj])
+        assert sd.r.shape == (n, 3)
+        ii = np.arange(n)
+        assert np.array_equal(sd.r.T, res.planes[:3, ii, jj], equal_nan=True)
+        assert np.array_equal(sd.v.T, res.planes[3:, ii, jj], equal_nan=True)
+        assert np.array_equal(sd.error_code, res.error[ii, jj])
