@@ -40,6 +40,9 @@
 #ifndef SGP4B_SMEM_REC
 #define SGP4B_SMEM_REC 0          // fp32 records in shared memory (default: registers)
 #endif
+#ifndef SGP4B_SHFL_REC
+#define SGP4B_SHFL_REC 0          // fp32 records spread over the warp (shfl at use)
+#endif
 #ifndef SGP4B_SMEM_REC64
 #define SGP4B_SMEM_REC64 1        // fp64 records (80 registers) in shared memory
 #endif
@@ -185,6 +188,17 @@ struct RecS {
 };
 template <>
 __device__ __forceinline__ int RecS<float>::flags() const { return __float_as_int(p[S_FLAGS]); }
+
+// a fp32 record spread over the warp: lane l holds fields l and 32 + l;
+// a field is broadcast with one shfl at use (2 registers per thread instead
+// of 40).  Requires the whole warp converged at every access.
+struct RecW {
+  float lo, hi;
+  __device__ __forceinline__ float operator[](int i) const {
+    return __shfl_sync(0xffffffffu, i < 32 ? lo : hi, i & 31);
+  }
+  __device__ __forceinline__ int flags() const { return __float_as_int((*this)[S_FLAGS]); }
+};
 template <>
 __device__ __forceinline__ int RecS<double>::flags() const {
   return (int)__double_as_longlong(p[S_FLAGS]);
@@ -1250,7 +1264,13 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
                                          int32_t* __restrict__ crow) {
   int64_t j0 = c0 * kCellsPerWarp + lane * kCellsPerLane;
   for (int64_t c = c0; c < c1; ++c, j0 += kCellsPerWarp) {
+#if SGP4B_SHFL_REC
+    // keep the warp converged (record fields are shuffled): lanes past the
+    // row end compute a dummy cell and skip the stores
+    if (__all_sync(0xffffffffu, j0 >= m)) break;
+#else
     if (j0 >= m) break;                     // only the row's last chunk is partial
+#endif
     T th[kCellsPerLane];
     float tl[kCellsPerLane];
     const bool full = VEC && j0 + kCellsPerLane <= m;
@@ -1356,17 +1376,23 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
   const int64_t g1 = total * (w + 1) / nwarps;
 
   constexpr bool kSmem = sizeof(T) == 8 ? SGP4B_SMEM_REC64 : SGP4B_SMEM_REC;
+  constexpr bool kShfl = sizeof(T) == 4 && SGP4B_SHFL_REC;
   __shared__ __align__(16) T srec[kSmem ? kGridBlock / 32 : 1][S_COUNT];
   T* my = srec[kSmem ? (threadIdx.x >> 5) : 0];
-  using RecT = typename std::conditional<kSmem, RecS<T>, Rec<T>>::type;
+  using RecT = typename std::conditional<
+      kShfl, RecW, typename std::conditional<kSmem, RecS<T>, Rec<T>>::type>::type;
   RecT R;
-  if constexpr (kSmem) R.p = my;
+  if constexpr (kSmem && !kShfl) R.p = my;
   for (int64_t gi = g0; gi < g1;) {
     const int64_t sat = gi / chunks;
     const int64_t c0 = gi - sat * chunks;
     const int64_t c1 = (g1 - gi < chunks - c0) ? c0 + (g1 - gi) : chunks;
     const int64_t ri = rec_idx != nullptr ? __ldg(rec_idx + sat) : sat;
-    if constexpr (kSmem) {
+    if constexpr (kShfl) {
+      const T* src = rec + ri * S_COUNT;
+      R.lo = __ldg(src + lane);
+      R.hi = lane + 32 < S_COUNT ? __ldg(src + 32 + lane) : 0.0f;
+    } else if constexpr (kSmem) {
       __syncwarp();
       for (int i = lane; i < S_COUNT; i += 32) my[i] = __ldg(rec + ri * S_COUNT + i);
       __syncwarp();
