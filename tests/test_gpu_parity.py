@@ -366,3 +366,57 @@ def test_randomized_grids(oracle, corpus_columns, seed):
         assert np.array_equal(sd.r.T, res.planes[:3, ii, jj], equal_nan=True)
         assert np.array_equal(sd.v.T, res.planes[3:, ii, jj], equal_nan=True)
         assert np.array_equal(sd.error_code, res.error[ii, jj])
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (3, 5), (33, 127), (5, 1001)])
+def test_fp32_odd_shapes_codes_and_bounds(oracle, corpus_columns, n, m):
+    """fp32 grids of unaligned width (padded device rows): codes equal the
+    reference at both precisions, errors bounded against the fp64 oracle."""
+    pkg = _gpu()
+    cols = corpus_columns[:, 7:7 + n]
+    times = np.linspace(-100.0, 3000.0, m)
+    res = pkg.propagate_batch(pkg.init_batch(cols, precision=32), times)
+    assert res.planes.shape == (6, n, m) and res.planes.flags["C_CONTIGUOUS"]
+    ref64, codes64 = oracle.grid(oracle.init_columns(cols, 64), times)
+    _, codes32 = oracle.grid(oracle.init_columns(cols, 32), times)
+    assert np.array_equal(res.error, codes64) and np.array_equal(res.error, codes32)
+    dr, _ = _diff(res.planes, ref64, codes64 == 0)
+    assert dr.max(initial=0) < 0.5
+
+
+def test_streamed_fp32_matches_dense(corpus_columns):
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :50], precision=32)
+    times = np.linspace(0.0, 2880.0, 301)
+    dense = pkg.propagate_batch(sats, times)
+    got = np.empty_like(dense.planes)
+    got_err = np.empty_like(dense.error)
+
+    def sink(rows, cols, planes, error):
+        assert planes.dtype == np.float32
+        got[:, rows, cols] = planes
+        got_err[rows, cols] = error
+
+    summary = pkg.propagate_batch_streamed(sats, times, tile_rows=17, tile_cols=64, sink=sink)
+    assert summary.cells_emitted == 50 * 301
+    assert np.array_equal(got, dense.planes) and np.array_equal(got_err, dense.error)
+
+
+def test_device_result_views_and_gather(corpus_columns):
+    """propagate_batch_device returns (6, N, M)/(N, M) views (rows padded to
+    4 steps); BatchResult.r/.v work on device tensors; shard gather on one
+    rank is the identity."""
+    import torch
+    from paper_2603_27830_b200.shard import gather_grid, propagate_sharded, shard_bounds
+    pkg = _gpu()
+    res = pkg.propagate_batch_device(pkg.init_batch(corpus_columns[:, :9], precision=32),
+                                     np.linspace(0.0, 100.0, 7))
+    assert tuple(res.planes.shape) == (6, 9, 7) and tuple(res.r.shape) == (9, 7, 3)
+    assert res.planes.stride(1) == 8          # padded row
+    host = pkg.propagate_batch(pkg.init_batch(corpus_columns[:, :9], precision=32),
+                               np.linspace(0.0, 100.0, 7))
+    assert np.array_equal(res.planes.cpu().numpy(), host.planes)
+    local, (lo, hi) = propagate_sharded(corpus_columns[:, :9], np.linspace(0.0, 100.0, 7))
+    assert (lo, hi) == shard_bounds(9, 1, 0) == (0, 9)
+    p, e = gather_grid(local.planes, local.error, 9)
+    assert torch.equal(p, local.planes) and torch.equal(e, local.error)

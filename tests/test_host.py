@@ -1,0 +1,114 @@
+"""Host-side logic that needs no GPU: scheduling helpers, the SGB1 binary
+format, gravity constants and API validation (mirrors pkg/tests/test_batch.py
+TestPartitionWork / TestTileGrid / TestBinaryFormat and gravity.py)."""
+
+import io
+import math
+
+import numpy as np
+import pytest
+
+from paper_2603_27830_b200 import (
+    WGS72,
+    BatchResult,
+    ErrorCode,
+    epoch_to_julian,
+    init_batch,
+    partition_work,
+    read_grid_binary,
+    write_grid_binary,
+)
+from paper_2603_27830_b200.batch import _tile_grid
+
+
+@pytest.mark.parametrize("n", range(1, 9))
+@pytest.mark.parametrize("m", range(1, 9))
+@pytest.mark.parametrize("workers", [1, 2, 3, 5, 8])
+def test_partition_work_disjoint_covering_balanced(n, m, workers):
+    ranges = partition_work(n, m, workers)
+    assert ranges[0][0] == 0 and ranges[-1][1] == n * m
+    for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+        assert a1 == b0 and a1 > a0
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1
+    assert len(ranges) == min(workers, n * m)
+
+
+def test_partition_work_rejects_zero_workers():
+    with pytest.raises(ValueError):
+        partition_work(4, 4, 0)
+
+
+def test_tile_grid_covers_exactly():
+    mask = np.zeros((10, 7), dtype=int)
+    for rows, cols in _tile_grid(10, 7, 4, 3):
+        mask[rows, cols] += 1
+    assert (mask == 1).all()
+
+
+def _fake_result(precision, n=3, m=5, seed=0):
+    rng = np.random.default_rng(seed)
+    dt = np.float32 if precision == 32 else np.float64
+    planes = rng.normal(size=(6, n, m)).astype(dt)
+    error = rng.integers(0, 7, size=(n, m)).astype(np.int32)
+    return BatchResult(planes=planes, error=error, n=n, m=m)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_sgb1_round_trip(precision):
+    res = _fake_result(precision)
+    buf = io.BytesIO()
+    write_grid_binary(res, buf)
+    buf.seek(0)
+    back = read_grid_binary(buf)
+    assert back.n == res.n and back.m == res.m
+    assert back.planes.dtype == res.planes.dtype
+    assert np.array_equal(back.planes, res.planes) and np.array_equal(back.error, res.error)
+
+
+def test_sgb1_header_layout():
+    res = _fake_result(32, n=2, m=3)
+    buf = io.BytesIO()
+    write_grid_binary(res, buf)
+    raw = buf.getvalue()
+    assert raw[:4] == b"SGB1"
+    assert int.from_bytes(raw[4:12], "little") == 2
+    assert int.from_bytes(raw[12:20], "little") == 3
+    assert int.from_bytes(raw[20:24], "little") == 32
+    assert raw[24:32] == b"rrrvvve\x00"
+    assert len(raw) == 32 + 6 * 2 * 3 * 4 + 2 * 3 * 4
+    with pytest.raises(ValueError):
+        read_grid_binary(io.BytesIO(b"NOPE" + b"\0" * 28))
+
+
+def test_wgs72_constants():
+    # gravity.py:31-47 of the reference, and the SURVEY §8(a) value of xke
+    assert WGS72.mu == 398600.8 and WGS72.radius_earth_km == 6378.135
+    assert WGS72.xke == pytest.approx(0.07436691613317342, rel=1e-15)
+    assert WGS72.xke == 60.0 / math.sqrt(6378.135 * 6378.135 * 6378.135 / 398600.8)
+    assert WGS72.tumin == 1.0 / WGS72.xke
+    assert WGS72.j3oj2 == WGS72.j3 / WGS72.j2
+    assert WGS72.as_array().shape == (8,)
+
+
+def test_error_code_values():
+    assert [int(c) for c in ErrorCode] == [0, 1, 2, 3, 4, 6, 7]
+
+
+def test_epoch_to_julian():
+    assert epoch_to_julian(2000, 1, 0.5) == 2451545.0
+    assert epoch_to_julian(1970, 1, 0.0) == 2440587.5
+    assert epoch_to_julian(2020, 366, 0.0) == epoch_to_julian(2021, 1, 0.0) - 1.0
+    with pytest.raises(ValueError):
+        epoch_to_julian(2021, 366, 0.0)
+
+
+def test_init_batch_validates_before_touching_the_gpu():
+    with pytest.raises(ValueError):
+        init_batch([])
+    with pytest.raises(ValueError):
+        init_batch(np.zeros((7, 0)))
+    with pytest.raises(ValueError):
+        init_batch(np.zeros((6, 3)))
+    with pytest.raises(ValueError):
+        init_batch(np.zeros((7, 3)), precision=16)
