@@ -102,13 +102,25 @@ enum Slot {
 };
 static_assert(S_COUNT == SGP4B_RECORD_SLOTS, "record slot count");
 
-// fp32 records re-purpose slots the fp32 cell does not read to hold
-// per-satellite products (computed in fp64 at pack time):
-constexpr int S32_NEG15CON41 = S_CON41;      // -1.5 con41
-constexpr int S32_HALFX1MTH2 = S_MDOT_LO;    //  0.5 x1mth2
-constexpr int S32_QX7THM1 = S_X7THM1;        // -0.25 x7thm1
-constexpr int S32_C15COSIO = S_ARGPDOT_LO;   //  1.5 cosio
-constexpr int S32_C15COSSIN = S_NODEDOT_LO;  //  1.5 cosio sinio
+// fp32 records have their own layout: per-satellite products the fp32 cell
+// would otherwise form per cell, computed in fp64 at pack time and rounded
+// once (store_record<float>).  The flags word sits at S_FLAGS in both.
+enum Slot32 {
+  P_MO = 0, P_MDOT, P_ARGPO, P_ARGPDOT, P_NODEO, P_NODEDOT, P_NODECF,
+  P_UDOT, P_UDOT_LO, P_U0,          // (mdot + argpdot) as hi + lo, (mo + argpo) in [-pi, pi)
+  P_A0, P_A1, P_A2, P_A3, P_OMGCOF, // delm: xmcof ((1 + eta x)^3 - delmo) = A0 + A1 x + A2 x^2 + A3 x^3
+  P_S, P_SC1, P_SD2, P_SD3, P_SD4,  // s, -s cc1, -s d2, -s d3, -s d4 with s = sqrt((xke/no)^(2/3))
+  P_N2, P_N3, P_N4, P_N5,           // no t2cof .. no t5cof
+  P_E0, P_BC4, P_BC5,               // ecco + bstar cc5 sinmao, bstar cc4, bstar cc5
+  P_AYCOF, P_XLCOF,
+  P_K41R, P_KXR, P_QX, P_C15CO,     // -1.5 con41 hj2 re, 0.5 x1mth2 hj2 re, -0.25 x7thm1 hj2, 1.5 cosio hj2
+  P_FLAGS,
+  P_C15CS, P_X1V, P_C41V,           // 1.5 cosio sinio hj2, x1mth2 hj2 vkm, 1.5 con41 hj2 vkm
+  P_SINIO, P_COSIO,
+  P_COUNT
+};
+static_assert(P_FLAGS == S_FLAGS, "fp32 flags slot");
+static_assert(P_COUNT <= S_COUNT, "fp32 record fits the packed slot count");
 
 // flags word
 constexpr int FLAG_ISIMP = 1;
@@ -651,10 +663,13 @@ __device__ __forceinline__ void rotate_tiny(VN<N> s, VN<N> c, VN<N> d, VN<N>& so
   co = fma2(c, cd, (-s) * d);
 }
 
-// Two fp32 cells of one satellite.  ISIMP and KITER are warp-uniform per
+// fp32 cells of one satellite.  ISIMP and KITER are warp-uniform per
 // satellite and compile-time here, so the cell is straight-line code.
 // KITER = 0: runtime Kepler count with a final SFU sincos (eccentric
-// orbits).  `R[i]` is the satellite's packed record (scalar fields).
+// orbits).  `R[i]` is the satellite's packed fp32 record (P_* slots): every
+// per-satellite product the reference forms per cell is pre-multiplied there
+// (in fp64, rounded once), including 0.5 j2, the Earth radius and the km/s
+// scale, so the cell spends its FP32 issue slots on per-cell work only.
 template <bool ISIMP, int KITER, bool LO, int NC, class RT>
 __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Grav& g,
                                       VN<NC> (&o)[6], int (&code)[NC]) {
@@ -665,43 +680,43 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   // secular gravity  kernel.py:366-370.  Only the Kepler argument needs the
   // double-float treatment: u = (mo + argpo) + (mdot + argpdot) t + ...
   // (mm + argpm; the drag term cancels), the rest enter sin/cos damped.
-  const V2 xmdf = fma2(t, R[S_MDOT], sp<NC>(R[S_MO]));
-  const V2 argpdf = fma2(t, R[S_ARGPDOT], sp<NC>(R[S_ARGPO]));
+  const V2 argpdf = fma2(t, R[P_ARGPDOT], sp<NC>(R[P_ARGPO]));
   const V2 t2 = t * t;
-  const V2 nodem = fma2(t2, R[S_NODECF], fma2(t, R[S_NODEDOT], sp<NC>(R[S_NODEO])));
-  const V2 ubase = secular_angle<LO, NC>(R[S_U0], R[S_UDOT], R[S_UDOT_LO], t, tl);
+  const V2 nodem = fma2(t2, R[P_NODECF], fma2(t, R[P_NODEDOT], sp<NC>(R[P_NODEO])));
+  const V2 ubase = secular_angle<LO, NC>(R[P_U0], R[P_UDOT], R[P_UDOT_LO], t, tl);
 
-  // drag  kernel.py:371-391; the t-polynomials in Horner form
-  V2 tempa, templ;
-  V2 tempe = t * R[S_BC4];
-  V2 temp = sp<NC>(0.0f);
+  // drag  kernel.py:371-391.  With s = sqrt((xke/no)^(2/3)) folded in,
+  // sqrt(am) = s tempa is one Horner polynomial in t; no templ is another.
+  V2 sqa, nol, argpm, em;
   if constexpr (ISIMP) {
-    tempa = fma2(t, -R[S_CC1], 1.0f);
-    templ = t2 * R[S_T2COF];
+    sqa = fma2(t, R[P_SC1], sp<NC>(R[P_S]));                       // s (1 - cc1 t)
+    nol = t2 * R[P_N2];                                            // no t2cof t^2
+    em = fma2(t, -R[P_BC4], sp<NC>(R[P_E0]));                     // ecco - bstar cc4 t
+    argpm = argpdf;
   } else {
+    const V2 xmdf = fma2(t, R[P_MDOT], sp<NC>(R[P_MO]));
     V2 sx, cx;
     sincos2(xmdf, sx, cx);
-    const V2 dmt = fma2(cx, R[S_ETA], 1.0f);
-    const V2 delm = fma2(dmt * dmt, dmt, sp<NC>(-R[S_DELMO])) * R[S_XMCOF];
-    temp = fma2(t, R[S_OMGCOF], delm);
-    // 1 - cc1 t - d2 t^2 - d3 t^3 - d4 t^4
-    tempa = fma2(t, fma2(t, fma2(t, fma2(t, -R[S_D4], -R[S_D3]), sp<NC>(-R[S_D2])),
-                         sp<NC>(-R[S_CC1])), 1.0f);
-    // t2cof t^2 + t3cof t^3 + t4cof t^4 + t5cof t^5
-    templ = t2 * fma2(t, fma2(t, fma2(t, R[S_T5COF], R[S_T4COF]), sp<NC>(R[S_T3COF])),
-                      sp<NC>(R[S_T2COF]));
-    // sin(xmdf + temp), temp the small drag correction of the mean anomaly
-    // (its square, times B* cc5, is far below fp32 resolution of em)
-    const V2 smm = fma2(cx, temp, sx);
-    tempe = fma2(smm - R[S_SINMAO], R[S_BC5], tempe);
+    // delomg + delm = omgcof t + xmcof ((1 + eta cos xmdf)^3 - delmo), the
+    // cubic expanded in cos xmdf (better conditioned than cubing 1 + eta cx)
+    const V2 temp = fma2(fma2(fma2(cx, R[P_A3], sp<NC>(R[P_A2])), cx, sp<NC>(R[P_A1])), cx,
+                         fma2(t, R[P_OMGCOF], sp<NC>(R[P_A0])));
+    // s (1 - cc1 t - d2 t^2 - d3 t^3 - d4 t^4)
+    sqa = fma2(t, fma2(t, fma2(t, fma2(t, R[P_SD4], sp<NC>(R[P_SD3])), sp<NC>(R[P_SD2])),
+                       sp<NC>(R[P_SC1])), sp<NC>(R[P_S]));
+    // no (t2cof t^2 + t3cof t^3 + t4cof t^4 + t5cof t^5)
+    nol = t2 * fma2(t, fma2(t, fma2(t, R[P_N5], sp<NC>(R[P_N4])), sp<NC>(R[P_N3])),
+                    sp<NC>(R[P_N2]));
+    // em = ecco - bstar cc4 t - bstar cc5 (sin(xmdf + temp) - sinmao), the
+    // sine expanded to first order in the small drag angle temp; E0 holds
+    // ecco + bstar cc5 sinmao
+    em = fma2(fma2(cx, temp, sx), -R[P_BC5], fma2(t, -R[P_BC4], sp<NC>(R[P_E0])));
+    argpm = argpdf - temp;
   }
-  const V2 argpm = argpdf - temp;
 
   // mean motion / eccentricity  kernel.py:397-408
-  const V2 am = vmax(tempa * tempa * R[S_AM0], tiny);        // maximum(am, tiny)
+  const V2 am = vmax(sqa * sqa, tiny);                            // maximum(am, tiny)
   const V2 rsam = rsq2(am);
-  const V2 rsam3 = rsam * rsam * rsam;                        // nm / xke = am^-1.5
-  V2 em = R[S_ECCO] - tempe;
   bool bad_em[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) bad_em[k] = (comp(em, k) >= 1.0f) || (comp(em, k) < -0.001f);
@@ -711,25 +726,48 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   V2 sa, ca;
   sincos2(argpm, sa, ca);
   const V2 axnl = em * ca;
-  const V2 ilp = rcp2(vmax(am * fma2(-em, em, 1.0f), tiny));
-  const V2 aynl = fma2(em, sa, ilp * R[S_AYCOF]);
+  const V2 rsam2 = rsam * rsam;                                   // 1 / am
+  V2 ilp;                                                         // 1 / pl_lp
+  if constexpr (KITER == 1) {
+    // e < 0.004 (+ drag margin): 1 / (am (1 - em^2)) = (1 + em^2) / am
+    // to O(em^4) < 1e-9, the guard pl_lp > tiny is implied
+    ilp = fma2(em, em, 1.0f) * rsam2;
+  } else {
+    ilp = rcp2(vmax(am * fma2(-em, em, 1.0f), tiny));
+  }
+  const V2 aynl = fma2(em, sa, ilp * R[P_AYCOF]);
   // u = xl - nodep = mm + argpm + (xlcof/pl) axnl  (mod 2pi)
-  const V2 u = fma2(ilp * R[S_XLCOF], axnl, fma2(templ, R[S_NO], ubase));
+  const V2 u = fma2(ilp * R[P_XLCOF], axnl, ubase + nol);
 
-  // Kepler, fixed warp-uniform iteration count  kernel.py:325-349
-  V2 eo1 = u, s = sp<NC>(0.0f), c = sp<NC>(1.0f), tem5 = sp<NC>(0.0f);
+  // Kepler, fixed warp-uniform iteration count  kernel.py:325-349.  E is
+  // carried as u + d so the residual u - E + axnl sinE - aynl cosE is formed
+  // without cancelling against u.
+  V2 s, c, d = sp<NC>(0.0f), tem5 = sp<NC>(0.0f);
+  V2 eo1 = u;
   const int kiter = KITER > 0 ? KITER : ((flags >> KEPLER_SHIFT) & 0xf);
 #pragma unroll
   for (int it = 0; it < (KITER > 0 ? KITER : 16); ++it) {
     if (KITER == 0 && it >= kiter) break;
-    sincos2(eo1, s, c);
-    const V2 den = fma2(-s, aynl, fma2(-c, axnl, 1.0f));
-    const V2 num = fma2(axnl, s, fma2(-aynl, c, u)) - eo1;
-    tem5 = num * rcp2(den);
+    sincos2(it == 0 ? u : (KITER > 0 ? u + d : eo1), s, c);
+    V2 num;
+    if constexpr (KITER > 0) {
+      num = it == 0 ? fma2(axnl, s, (-aynl) * c) : fma2(axnl, s, fma2(-aynl, c, -d));
+    } else {
+      num = fma2(axnl, s, fma2(-aynl, c, u)) - eo1;
+    }
+    if constexpr (KITER == 1) {
+      // den = 1 - q with |q| <= e < 0.004: 1/den = 1 + q + q^2 to O(q^3)
+      const V2 q = fma2(c, axnl, s * aynl);
+      tem5 = num * fma2(q, q + 1.0f, 1.0f);
+    } else {
+      const V2 den = fma2(-s, aynl, fma2(-c, axnl, 1.0f));
+      tem5 = num * rcp2(den);
+    }
     // the +-0.95 clamp (kernel.py:343-346) cannot trigger for e < 0.1
     // (|num| <= 2e, den >= 1 - 2e), i.e. for KITER 1 and 2
     if (KITER == 0 || KITER > 2) tem5 = clamp95(tem5);
-    eo1 = eo1 + tem5;
+    if constexpr (KITER > 0) d = it == 0 ? tem5 : d + tem5;
+    else eo1 = eo1 + tem5;
   }
   V2 sineo1, coseo1;
   if constexpr (KITER > 0) {
@@ -742,81 +780,89 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 ecose = fma2(axnl, coseo1, aynl * sineo1);
   const V2 esine = fma2(axnl, sineo1, (-aynl) * coseo1);
   const V2 el2 = fma2(axnl, axnl, aynl * aynl);
-  const V2 pl = am * (1.0f - el2);
+  const V2 omel2 = 1.0f - el2;
   bool bad_pl[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) bad_pl[k] = comp(pl, k) < 0.0f;
-  const V2 pl_safe = vmax(pl, tiny);
   const V2 rl = am * (1.0f - ecose);
   const V2 irl = rcp2(nonzero(rl, tiny));
-  const V2 sqam = am * rsam;                               // sqrt(am)
-  const V2 rdotl = sqam * esine * irl;                     // sqrt(am) esine / rl
-  V2 rvdotl, betal, tq, ipl;
-#ifndef SGP4B_SERIES
-#define SGP4B_SERIES 0
-#endif
-  if constexpr (SGP4B_SERIES && (KITER == 1 || KITER == 2)) {
-    // e < 0.1 so x = el2 < 0.012: sqrt(1-x), 1/(1+sqrt(1-x)) and 1/(1-x)
-    // as series in x (truncation < 1e-8 relative); pl > 0 here.
-    const V2 x = el2;
-    betal = fma2(x, fma2(x, fma2(x, -0.0625f, -0.125f), -0.5f), 1.0f);
-    tq = esine * fma2(x, fma2(x, fma2(x, 0.0390625f, 0.0625f), 0.125f), 0.5f);
-    rvdotl = sqam * betal * irl;                           // sqrt(am (1-x)) / rl
-    ipl = (rsam * rsam) * fma2(x, fma2(x, x + 1.0f, 1.0f), 1.0f);
-  } else if constexpr (KITER == 1 || KITER == 2) {
-    // e < 0.1: pl = am (1 - el2) > 0, so 1/sqrt(pl) = rsqrt(am) / betal and
-    // one SFU rsqrt serves betal, sqrt(pl) and 1/pl
-    const V2 omel2 = 1.0f - el2;
+  const V2 nrm = am * irl;                                 // am / rl
+  V2 betal, tq, ipl;
+  if constexpr (KITER == 1) {
+    // x = el2 < 2e-5: sqrt(1-x), 1/sqrt(1-x) and 1/(1 + sqrt(1-x)) as
+    // first-order series (truncation < 4e-9 even at e = 0.01); pl < 0 iff
+    // el2 > 1
+#pragma unroll
+    for (int k = 0; k < NC; ++k) bad_pl[k] = comp(el2, k) > 1.0f;
+    betal = fma2(el2, -0.5f, 1.0f);
+    tq = esine * fma2(el2, 0.125f, 0.5f);
+    const V2 rspl = rsam * fma2(el2, 0.5f, 1.0f);
+    ipl = rspl * rspl;
+  } else if constexpr (KITER == 2) {
+    // e < 0.1: pl = am (1 - el2), and am > 0, so the sign test of pl is
+    // that of 1 - el2; one SFU rsqrt serves betal, sqrt(pl) and 1/pl
+#pragma unroll
+    for (int k = 0; k < NC; ++k) bad_pl[k] = comp(omel2, k) < 0.0f;
     const V2 rb = rsq2(omel2);
     betal = omel2 * rb;
-    rvdotl = sqam * betal * irl;                           // sqrt(pl) / rl
     tq = esine * rcp2(betal + 1.0f);
     const V2 rspl = rsam * rb;
     ipl = rspl * rspl;
   } else {
-    const V2 rspl = rsq2(pl_safe);
-    rvdotl = (pl_safe * rspl) * irl;                       // sqrt(pl) / rl
-    const V2 omel2 = vmax(1.0f - el2, tiny);
-    betal = omel2 * rsq2(omel2);
+    const V2 pl = am * omel2;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) bad_pl[k] = comp(pl, k) < 0.0f;
+    const V2 rspl = rsq2(vmax(pl, tiny));
+    const V2 ob = vmax(omel2, tiny);
+    betal = ob * rsq2(ob);
     tq = esine * rcp2(betal + 1.0f);
+    // sqrt(pl_safe) / rl = (am/rl) betal when pl > tiny; otherwise use the
+    // guarded form
     ipl = rspl * rspl;
+  }
+  // sqrt(am) / rl and sqrt(pl) / rl in km/s: (am/rl) (vkm / sqrt(am))
+  const V2 sqv = nrm * (rsam * g.vkm_f);
+  const V2 rdv = sqv * esine;                              // rdotl vkm
+  V2 rvdv = sqv * betal;                                   // rvdotl vkm
+  if constexpr (KITER == 0 || KITER > 2) {
+    // general orbits: sqrt(pl_safe) may differ from sqrt(am) betal
+    const V2 pl = am * omel2;
+    const V2 pls = vmax(pl, tiny);
+    rvdv = (pls * rsq2(pls)) * (irl * g.vkm_f);
   }
   // (sin u, cos u) = (am/rl) (sn, cs)  (kernel.py:453-454); the atan2 of
   // :455 is only ever used through sin/cos, so no angle is formed.
-  const V2 nrm = am * irl;
   const V2 sinu = fma2(-axnl, tq, sineo1 - aynl) * nrm;
   const V2 cosu = fma2(aynl, tq, coseo1 - axnl) * nrm;
-  const V2 sin2u = (cosu + cosu) * sinu;
-  const V2 cos2u = fma2(sinu * -2.0f, sinu, 1.0f);
-  const V2 temp1 = ipl * g.half_j2_f;
-  const V2 temp2 = temp1 * ipl;
+  const V2 s2u = sinu + sinu;
+  const V2 sin2u = s2u * cosu;
+  const V2 cos2u = fma2(-s2u, sinu, 1.0f);
+  const V2 ipl2 = ipl * ipl;                               // temp2 / (0.5 j2)
 
-  // short-period periodics  kernel.py:463-469 (per-satellite factors
-  // pre-multiplied in the record)
-  const float n15c41 = R[S32_NEG15CON41], x1mth2 = R[S_X1MTH2];
-  const V2 mrt = fma2(rl, fma2(temp2 * n15c41, betal, 1.0f), (temp1 * R[S32_HALFX1MTH2]) * cos2u);
-  const V2 t2s = temp2 * sin2u;
-  const V2 dsu = t2s * R[S32_QX7THM1];
-  const V2 dinc = (temp2 * cos2u) * R[S32_C15COSSIN];
-  const V2 nmt = rsam3 * temp1;                            // nm temp1 / xke
-  const V2 mvt = fma2((-nmt) * x1mth2, sin2u, rdotl);
-  const V2 rvdot = fma2(nmt, fma2(cos2u, x1mth2, sp<NC>(-n15c41)), rvdotl);
+  // short-period periodics  kernel.py:463-469 (0.5 j2, re and the km/s
+  // scale pre-multiplied into the record's per-satellite factors)
+  const V2 mr = fma2(rl, fma2(ipl2 * R[P_K41R], betal, sp<NC>(g.re_f)), (ipl * R[P_KXR]) * cos2u);
+  const V2 t2s = ipl2 * sin2u;
+  const V2 dsu = t2s * R[P_QX];
+  const V2 dinc = (ipl2 * cos2u) * R[P_C15CS];
+  const V2 nmt = rsam2 * rsam * ipl;                       // nm temp1 / (xke 0.5 j2)
+  const V2 mv = fma2(-(nmt * R[P_X1V]), sin2u, rdv);
+  const V2 rv = fma2(nmt, fma2(cos2u, R[P_X1V], sp<NC>(R[P_C41V])), rvdv);
 
   // orientation  kernel.py:472-493
   V2 sinsu, cossu, snod, cnod, sini, cosi;
   rotate_tiny(sinu, cosu, dsu, sinsu, cossu);
-  sincos2(fma2(t2s, R[S32_C15COSIO], nodem), snod, cnod);   // xnode
-  rotate_tiny(sp<NC>(R[S_SINIO]), sp<NC>(R[S_COSIO]), dinc, sini, cosi);
+  sincos2(fma2(t2s, R[P_C15CO], nodem), snod, cnod);     // xnode
+  // xinc = inclo + dinc with |dinc| <= 1.5 temp2 |cos i sin i| < 4e-4: the
+  // second-order term dinc^2/2 < 8e-8 is below fp32 resolution of r and v
+  sini = fma2(dinc, R[P_COSIO], sp<NC>(R[P_SINIO]));
+  cosi = fma2(dinc, -R[P_SINIO], sp<NC>(R[P_COSIO]));
   // r = mr U, v = mv U + rv V with U, V the orientation vectors; grouped as
   // r = (xm, cnod|snod, sini) . (mr sinsu, mr cossu), same for v
   const V2 xmx = (-snod) * cosi;
   const V2 xmy = cnod * cosi;
-  const V2 mr = mrt * g.re_f;
   const V2 ra = mr * sinsu, rb = mr * cossu;
   o[0] = fma2(xmx, ra, cnod * rb);
   o[1] = fma2(xmy, ra, snod * rb);
   o[2] = sini * ra;
-  const V2 mv = mvt * g.vkm_f, rv = rvdot * g.vkm_f;
   const V2 va = fma2(mv, sinsu, rv * cossu);
   const V2 vb = fma2(mv, cossu, (-rv) * sinsu);
   o[3] = fma2(xmx, va, cnod * vb);
@@ -824,10 +870,11 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   o[5] = sini * va;
 
   // _first_error 2 > 1 > 4 > 6 and the init merge  kernel.py:497-502, 529-534
+  // (decayed: mrt < 1 earth radius, i.e. mr < re)
   const int persistent = (flags >> CODE_SHIFT) & 0xff;     // includes bad_nm -> 2
 #pragma unroll
   for (int h = 0; h < NC; ++h) {
-    const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (comp(mrt, h) < 1.0f) ? 6 : 0;
+    const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (comp(mr, h) < g.re_f) ? 6 : 0;
     code[h] = persistent != 0 ? persistent : cellc;
   }
 }
@@ -922,31 +969,70 @@ __device__ __forceinline__ void store_record<double>(const double* f, int init_c
   for (int i = 0; i < S_COUNT; ++i) rec[i] = v[i];
 }
 
+// reduce an angle to [-pi, pi): fp32 has the most resolution there
+__device__ __forceinline__ double signed_2pi(double x) {
+  const double r = pymod_2pi(x);
+  return r >= kPi ? r - kTwoPi : r;
+}
+
 template <>
 __device__ __forceinline__ void store_record<float>(const double* f, int init_code, bool isimp,
                                                     const Grav& g, float* __restrict__ rec) {
   double v[S_COUNT];
   int flags;
   record_values(f, init_code, isimp, g, v, flags);
-  float o[S_COUNT];
+  double o[S_COUNT];
 #pragma unroll
-  for (int i = 0; i < S_COUNT; ++i) o[i] = (float)v[i];
-  split_df(v[S_UDOT], o[S_UDOT], o[S_UDOT_LO]);
-  o[S32_NEG15CON41] = (float)(-1.5 * f[F_CON41]);
-  o[S32_HALFX1MTH2] = (float)(0.5 * f[F_X1MTH2]);
-  o[S32_QX7THM1] = (float)(-0.25 * f[F_X7THM1]);
-  o[S32_C15COSIO] = (float)(1.5 * v[S_COSIO]);
-  o[S32_C15COSSIN] = (float)(1.5 * v[S_COSIO] * v[S_SINIO]);
-  // angles that only meet sin/cos or the Kepler argument: keep them in
-  // [-pi, pi) where fp32 has the most resolution
-  o[S_U0] = (float)(v[S_U0] >= kPi ? v[S_U0] - kTwoPi : v[S_U0]);
-  {
-    const double nd = pymod_2pi(v[S_NODEO]);
-    o[S_NODEO] = (float)(nd >= kPi ? nd - kTwoPi : nd);
+  for (int i = 0; i < S_COUNT; ++i) o[i] = 0.0;
+  const double hj2 = 0.5 * g.j2, bstar = f[F_BSTAR], no = v[S_NO];
+  const double s = sqrt(v[S_AM0]);
+  o[P_MO] = signed_2pi(f[F_MO]);
+  o[P_MDOT] = f[F_MDOT];
+  o[P_ARGPO] = signed_2pi(f[F_ARGPO]);
+  o[P_ARGPDOT] = f[F_ARGPDOT];
+  o[P_NODEO] = signed_2pi(f[F_NODEO]);
+  o[P_NODEDOT] = f[F_NODEDOT];
+  o[P_NODECF] = f[F_NODECF];
+  o[P_U0] = signed_2pi(v[S_U0]);
+  o[P_S] = s;
+  o[P_SC1] = -s * f[F_CC1];
+  o[P_N2] = no * f[F_T2COF];
+  o[P_E0] = f[F_ECCO];
+  o[P_BC4] = bstar * f[F_CC4];
+  if (!isimp) {                       // kernel.py:371-391 (zero in isimp records)
+    const double eta = f[F_ETA], xmcof = f[F_XMCOF];
+    o[P_A0] = xmcof * (1.0 - f[F_DELMO]);
+    o[P_A1] = 3.0 * xmcof * eta;
+    o[P_A2] = 3.0 * xmcof * eta * eta;
+    o[P_A3] = xmcof * eta * eta * eta;
+    o[P_OMGCOF] = f[F_OMGCOF];
+    o[P_SD2] = -s * f[F_D2];
+    o[P_SD3] = -s * f[F_D3];
+    o[P_SD4] = -s * f[F_D4];
+    o[P_N3] = no * f[F_T3COF];
+    o[P_N4] = no * f[F_T4COF];
+    o[P_N5] = no * f[F_T5COF];
+    o[P_BC5] = bstar * f[F_CC5];
+    o[P_E0] = f[F_ECCO] + bstar * f[F_CC5] * f[F_SINMAO];
   }
-  o[S_FLAGS] = __int_as_float(flags);
+  o[P_AYCOF] = f[F_AYCOF];
+  o[P_XLCOF] = f[F_XLCOF];
+  o[P_K41R] = -1.5 * f[F_CON41] * hj2 * g.re;
+  o[P_KXR] = 0.5 * f[F_X1MTH2] * hj2 * g.re;
+  o[P_QX] = -0.25 * f[F_X7THM1] * hj2;
+  o[P_C15CO] = 1.5 * v[S_COSIO] * hj2;
+  o[P_C15CS] = 1.5 * v[S_COSIO] * v[S_SINIO] * hj2;
+  o[P_X1V] = f[F_X1MTH2] * hj2 * g.vkm;
+  o[P_C41V] = 1.5 * f[F_CON41] * hj2 * g.vkm;
+  o[P_SINIO] = v[S_SINIO];
+  o[P_COSIO] = v[S_COSIO];
+  float r[S_COUNT];
 #pragma unroll
-  for (int i = 0; i < S_COUNT; ++i) rec[i] = o[i];
+  for (int i = 0; i < S_COUNT; ++i) r[i] = (float)o[i];
+  split_df(v[S_UDOT], r[P_UDOT], r[P_UDOT_LO]);
+  r[P_FLAGS] = __int_as_float(flags);
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) rec[i] = r[i];
 }
 
 // ======================================================================
@@ -1147,14 +1233,20 @@ __device__ __forceinline__ void st_cs(int32_t* p, int32_t v) { __stcs(reinterpre
 // vector streaming stores / read-only loads of N consecutive elements
 template <int N>
 __device__ __forceinline__ void st_vec_cs(float* p, const float (&v)[N]) {
-  if constexpr (N == 4) __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
-  else if constexpr (N == 2) __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < N; k += 4)
+      __stcs(reinterpret_cast<float4*>(p + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+  } else if constexpr (N == 2) __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
   else for (int k = 0; k < N; ++k) __stcs(p + k, v[k]);
 }
 template <int N>
 __device__ __forceinline__ void st_vec_cs(int32_t* p, const int (&v)[N]) {
-  if constexpr (N == 4) __stcs(reinterpret_cast<int4*>(p), make_int4(v[0], v[1], v[2], v[3]));
-  else if constexpr (N == 2) __stcs(reinterpret_cast<int2*>(p), make_int2(v[0], v[1]));
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < N; k += 4)
+      __stcs(reinterpret_cast<int4*>(p + k), make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+  } else if constexpr (N == 2) __stcs(reinterpret_cast<int2*>(p), make_int2(v[0], v[1]));
   else for (int k = 0; k < N; ++k) __stcs(reinterpret_cast<int*>(p) + k, v[k]);
 }
 template <int N>
@@ -1166,9 +1258,12 @@ __device__ __forceinline__ void st_vec_cs(double* p, const double (&v)[N]) {
 }
 template <int N>
 __device__ __forceinline__ void ld_vec(const float* p, float (&v)[N]) {
-  if constexpr (N == 4) {
-    float4 q = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < N; k += 4) {
+      float4 q = __ldg(reinterpret_cast<const float4*>(p + k));
+      v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+    }
   } else if constexpr (N == 2) {
     float2 q = __ldg(reinterpret_cast<const float2*>(p));
     v[0] = q.x; v[1] = q.y;
@@ -1286,6 +1381,21 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     T out[6][kCellsPerLane];
     int code[kCellsPerLane];
     cells(th, tl, out, code);
+#ifdef SGP4B_NOSTORE
+    // analysis build: compute-only timing (results kept alive, never stored)
+    {
+      T acc = T(0);
+      int ca = 0;
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) {
+#pragma unroll
+        for (int p = 0; p < 6; ++p) acc += out[p][k];
+        ca |= code[k];
+      }
+      if (acc == T(1.2345e-30) && ca == 77) st_cs(row + j0, acc);
+      continue;
+    }
+#endif
 
     T* base = row + j0;
     int32_t* cbase = crow + j0;
@@ -1322,6 +1432,12 @@ template <bool VEC, bool LO, class RT>
 __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t c0, int64_t c1,
                                              int lane, const float* times, const float* times_lo,
                                              int64_t m, float* row, int64_t ps, int32_t* crow) {
+#ifdef SGP4B_ONLY_CLASS_K1
+  // analysis build: every row runs the (non-isimp, Kepler 1) instance, so the
+  // SASS holds one chunk loop (static instruction mix per cell)
+  row32<false, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  return;
+#endif
   const int flags = R.flags();
   const int kit = (flags >> KEPLER_SHIFT) & 0xf;
   if (!(flags & FLAG_ISIMP)) {
