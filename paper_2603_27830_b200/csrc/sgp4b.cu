@@ -68,6 +68,7 @@ constexpr double kPi = 3.14159265358979323846264338327950;
 constexpr float kTwoPiHiF = 6.28318548202514648437f;     // float(2*pi)
 constexpr float kTwoPiLoF = -1.7484556000744487e-07f;    // 2*pi - hi
 constexpr float kInvTwoPiF = 0.159154943091895335768883763372514f;
+constexpr float kRoundMagicF = 12582912.0f;                // 1.5 * 2^23
 
 struct Grav {
   double mu, re, xke, tumin, j2, j3, j4, j3oj2;
@@ -647,7 +648,8 @@ __device__ __forceinline__ VN<N> secular_angle(float x0, float rate, float rate_
   VN<N> e = fma2(t, rate, -p);
   e = fma2(t, rate_lo, e);
   if constexpr (LO) e = fma2(tl, rate, e);
-  const VN<N> k = rint2(p * kInvTwoPiF);
+  // k = rint(p / 2pi) by the 1.5 2^23 shifter (packed, |p / 2pi| < 2^22)
+  const VN<N> k = fma2(p, kInvTwoPiF, kRoundMagicF) - kRoundMagicF;
   VN<N> r = fma2(-k, kTwoPiHiF, p);
   r = fma2(-k, kTwoPiLoF, r);
   return r + (e + x0);
@@ -699,8 +701,16 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     sincos2(xmdf, sx, cx);
     // delomg + delm = omgcof t + xmcof ((1 + eta cos xmdf)^3 - delmo), the
     // cubic expanded in cos xmdf (better conditioned than cubing 1 + eta cx)
-    const V2 temp = fma2(fma2(fma2(cx, R[P_A3], sp<NC>(R[P_A2])), cx, sp<NC>(R[P_A1])), cx,
-                         fma2(t, R[P_OMGCOF], sp<NC>(R[P_A0])));
+    V2 temp;
+    if constexpr (KITER == 1) {
+      // e < 0.003: eta = ao e tsi < 0.06, so the eta^2, eta^3 terms are below
+      // 3e-7 rad of the small drag angle, which only reaches r through
+      // em sin/cos(argpm) (< 1e-7 m)
+      temp = fma2(cx, R[P_A1], fma2(t, R[P_OMGCOF], sp<NC>(R[P_A0])));
+    } else {
+      temp = fma2(fma2(fma2(cx, R[P_A3], sp<NC>(R[P_A2])), cx, sp<NC>(R[P_A1])), cx,
+                  fma2(t, R[P_OMGCOF], sp<NC>(R[P_A0])));
+    }
     // s (1 - cc1 t - d2 t^2 - d3 t^3 - d4 t^4)
     sqa = fma2(t, fma2(t, fma2(t, fma2(t, R[P_SD4], sp<NC>(R[P_SD3])), sp<NC>(R[P_SD2])),
                        sp<NC>(R[P_SC1])), sp<NC>(R[P_S]));
@@ -782,9 +792,9 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 el2 = fma2(axnl, axnl, aynl * aynl);
   const V2 omel2 = 1.0f - el2;
   bool bad_pl[NC];
-  const V2 rl = am * (1.0f - ecose);
-  const V2 irl = rcp2(nonzero(rl, tiny));
-  const V2 nrm = am * irl;                                 // am / rl
+  const V2 ome = 1.0f - ecose;
+  const V2 rl = am * ome;
+  const V2 nrm = rcp2(nonzero(ome, tiny));                 // am / rl (am > 0)
   V2 betal, tq, ipl;
   if constexpr (KITER == 1) {
     // x = el2 < 2e-5: sqrt(1-x), 1/sqrt(1-x) and 1/(1 + sqrt(1-x)) as
@@ -794,8 +804,7 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     for (int k = 0; k < NC; ++k) bad_pl[k] = comp(el2, k) > 1.0f;
     betal = fma2(el2, -0.5f, 1.0f);
     tq = esine * fma2(el2, 0.125f, 0.5f);
-    const V2 rspl = rsam * fma2(el2, 0.5f, 1.0f);
-    ipl = rspl * rspl;
+    ipl = fma2(rsam2, el2, rsam2);                         // (1 + el2) / am
   } else if constexpr (KITER == 2) {
     // e < 0.1: pl = am (1 - el2), and am > 0, so the sign test of pl is
     // that of 1 - el2; one SFU rsqrt serves betal, sqrt(pl) and 1/pl
@@ -826,7 +835,7 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     // general orbits: sqrt(pl_safe) may differ from sqrt(am) betal
     const V2 pl = am * omel2;
     const V2 pls = vmax(pl, tiny);
-    rvdv = (pls * rsq2(pls)) * (irl * g.vkm_f);
+    rvdv = (pls * rsq2(pls)) * (nrm * (rsam2 * g.vkm_f));  // sqrt(pl) / rl
   }
   // (sin u, cos u) = (am/rl) (sn, cs)  (kernel.py:453-454); the atan2 of
   // :455 is only ever used through sin/cos, so no angle is formed.
@@ -839,7 +848,10 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
 
   // short-period periodics  kernel.py:463-469 (0.5 j2, re and the km/s
   // scale pre-multiplied into the record's per-satellite factors)
-  const V2 mr = fma2(rl, fma2(ipl2 * R[P_K41R], betal, sp<NC>(g.re_f)), (ipl * R[P_KXR]) * cos2u);
+  // mr = re mrt; for e < 0.003 betal = 1 - O(1e-5) in the J2 term (< 1e-8)
+  const V2 k41 = KITER == 1 ? fma2(ipl2, R[P_K41R], sp<NC>(g.re_f))
+                            : fma2(ipl2 * R[P_K41R], betal, sp<NC>(g.re_f));
+  const V2 mr = fma2(rl, k41, (ipl * R[P_KXR]) * cos2u);
   const V2 t2s = ipl2 * sin2u;
   const V2 dsu = t2s * R[P_QX];
   const V2 dinc = (ipl2 * cos2u) * R[P_C15CS];
@@ -1357,7 +1369,21 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
                                          const float* __restrict__ times_lo, int64_t m,
                                          T* __restrict__ row, int64_t plane_stride,
                                          int32_t* __restrict__ crow) {
+  // a lane's kCellsPerLane times at column j (zero past the row end)
+  auto load_times = [&](int64_t j, T (&th)[kCellsPerLane], float (&tl)[kCellsPerLane]) {
+    if (VEC && j + kCellsPerLane <= m) {
+      ld_vec<kCellsPerLane>(times + j, th);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) th[k] = j + k < m ? __ldg(times + j + k) : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j + k < m) ? __ldg(times_lo + j + k) : 0.0f;
+  };
   int64_t j0 = c0 * kCellsPerWarp + lane * kCellsPerLane;
+  T th[kCellsPerLane];
+  float tl[kCellsPerLane];
+  load_times(j0, th, tl);
   for (int64_t c = c0; c < c1; ++c, j0 += kCellsPerWarp) {
 #if SGP4B_SHFL_REC
     // keep the warp converged (record fields are shuffled): lanes past the
@@ -1366,17 +1392,12 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
 #else
     if (j0 >= m) break;                     // only the row's last chunk is partial
 #endif
-    T th[kCellsPerLane];
-    float tl[kCellsPerLane];
     const bool full = VEC && j0 + kCellsPerLane <= m;
-    if (full) {
-      ld_vec<kCellsPerLane>(times + j0, th);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kCellsPerLane; ++k) th[k] = j0 + k < m ? __ldg(times + j0 + k) : T(0);
-    }
-#pragma unroll
-    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j0 + k < m) ? __ldg(times_lo + j0 + k) : 0.0f;
+    // the next chunk's times are loaded before this chunk's cells run, so
+    // their latency hides behind the cell math
+    T thn[kCellsPerLane];
+    float tln[kCellsPerLane];
+    load_times(j0 + kCellsPerWarp, thn, tln);
 
     T out[6][kCellsPerLane];
     int code[kCellsPerLane];
@@ -1393,6 +1414,11 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
         ca |= code[k];
       }
       if (acc == T(1.2345e-30) && ca == 77) st_cs(row + j0, acc);
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) {
+        th[k] = thn[k];
+        tl[k] = tln[k];
+      }
       continue;
     }
 #endif
@@ -1412,6 +1438,11 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
           st_cs(cbase + k, code[k]);
         }
       }
+    }
+#pragma unroll
+    for (int k = 0; k < kCellsPerLane; ++k) {
+      th[k] = thn[k];
+      tl[k] = tln[k];
     }
   }
 }
@@ -1515,6 +1546,9 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
     } else {
       load_rec(rec + ri * S_COUNT, R);
     }
+    // pull the next row's record toward L1 while this row computes
+    if (rec_idx == nullptr && gi + (c1 - c0) < g1 && lane < (int)(S_COUNT * sizeof(T) + 127) / 128)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (ri + 1) * S_COUNT + lane * (128 / sizeof(T))));
     dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
                      LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
                      plane_stride, codes + sat * code_stride);
@@ -1542,13 +1576,16 @@ __global__ void drift_norms_kernel(const float* __restrict__ p32, const double* 
     dv[i] = CUDART_INF;
     return;
   }
+  // np.linalg.norm(x, axis=-1) as drift.py:71-72 evaluates it: squares
+  // rounded, then summed left to right (no fused multiply-add), so the
+  // percentiles match a NumPy recomputation bit for bit
   double r2 = 0.0, v2 = 0.0;
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
     const double a = (double)__ldg(p32 + p * cells + i) - __ldg(p64 + p * cells + i);
     const double b = (double)__ldg(p32 + (p + 3) * cells + i) - __ldg(p64 + (p + 3) * cells + i);
-    r2 = fma(a, a, r2);
-    v2 = fma(b, b, v2);
+    r2 = p == 0 ? __dmul_rn(a, a) : __dadd_rn(r2, __dmul_rn(a, a));
+    v2 = p == 0 ? __dmul_rn(b, b) : __dadd_rn(v2, __dmul_rn(b, b));
   }
   dr[i] = sqrt(r2);
   dv[i] = sqrt(v2);
