@@ -107,7 +107,8 @@ static_assert(S_COUNT == SGP4B_RECORD_SLOTS, "record slot count");
 // would otherwise form per cell, computed in fp64 at pack time and rounded
 // once (store_record<float>).  The flags word sits at S_FLAGS in both.
 enum Slot32 {
-  P_MO = 0, P_MDOT, P_ARGPO, P_ARGPDOT, P_NODEO, P_NODEDOT, P_NODECF,
+  P_MO = 0, P_MDOT,                 // kept for inspection; the cell derives xmdf from U0/UDOT
+  P_ARGPO, P_ARGPDOT, P_NODEO, P_NODEDOT, P_NODECF,
   P_UDOT, P_UDOT_LO, P_U0,          // (mdot + argpdot) as hi + lo, (mo + argpo) in [-pi, pi)
   P_A0, P_A1, P_A2, P_A3, P_OMGCOF, // delm: xmcof ((1 + eta x)^3 - delmo) = A0 + A1 x + A2 x^2 + A3 x^3
   P_S, P_SC1, P_SD2, P_SD3, P_SD4,  // s, -s cc1, -s d2, -s d3, -s d4 with s = sqrt((xke/no)^(2/3))
@@ -696,7 +697,9 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     em = fma2(t, -R[P_BC4], sp<NC>(R[P_E0]));                     // ecco - bstar cc4 t
     argpm = argpdf;
   } else {
-    const V2 xmdf = fma2(t, R[P_MDOT], sp<NC>(R[P_MO]));
+    // xmdf = mo + mdot t = (mo + argpo + (mdot + argpdot) t) - argpdf,
+    // from the reduced Kepler argument: a small angle for the SFU
+    const V2 xmdf = ubase - argpdf;
     V2 sx, cx;
     sincos2(xmdf, sx, cx);
     // delomg + delm = omgcof t + xmcof ((1 + eta cos xmdf)^3 - delmo), the
@@ -1530,6 +1533,12 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
       kShfl, RecW, typename std::conditional<kSmem, RecS<T>, Rec<T>>::type>::type;
   RecT R;
   if constexpr (kSmem && !kShfl) R.p = my;
+  if (g0 < g1) {
+    // the first chunk's times travel with the first record load
+    const int64_t s0 = g0 / chunks;
+    const int64_t jf = (g0 - s0 * chunks) * kCellsPerWarp + lane * kCellsPerLane;
+    if (jf < m) asm volatile("prefetch.global.L1 [%0];" ::"l"(times + s0 * times_ld + jf));
+  }
   for (int64_t gi = g0; gi < g1;) {
     const int64_t sat = gi / chunks;
     const int64_t c0 = gi - sat * chunks;
