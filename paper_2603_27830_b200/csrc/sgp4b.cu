@@ -101,6 +101,9 @@ enum Slot {
   S_MDOT_LO, S_ARGPDOT_LO, S_NODEDOT_LO, S_UDOT, S_UDOT_LO, S_U0,
   S_COUNT
 };
+// fp64 records re-use the (fp32-only) low-word slots
+constexpr int S64_SQAM0 = S_MDOT_LO;       // sqrt((xke/no)^(2/3))
+constexpr int S64_NOSAFE = S_ARGPDOT_LO;   // xke / am0^1.5 (= no, or 1e-4 if no <= 0)
 static_assert(S_COUNT == SGP4B_RECORD_SLOTS, "record slot count");
 
 // fp32 records have their own layout: per-satellite products the fp32 cell
@@ -326,21 +329,13 @@ __device__ __forceinline__ void sincos64(double x, double* sp, double* cp) {
   *cp = ((q + 1) & 2) ? -c0 : c0;
 }
 
-// 1/x and a/b: SFU seed + two Newton steps + one residual correction
+// 1/x by one third-order step r (1 + e + e^2), e = 1 - x r, from the SFU
+// seed (|e| ~ 2^-22, so the result error e^3 is below fp64 rounding)
 __device__ __forceinline__ double rcp64(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ double div64(double a, double b) {
-  const double r = rcp64(b);
-  const double q = a * r;
-  return fma(r, fma(-b, q, a), q);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);              // r (1 + e + e^2)
 }
 // sqrt(x) and 1/sqrt(x) for x > 0: SFU rsqrt seed + Newton, then a
 // Tuckerman-style correction of x * (1/sqrt x)
@@ -348,8 +343,7 @@ __device__ __forceinline__ double rsqrt64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);                // ~2^-22 -> 2^-43 -> fp64
   return y * fma(-hx * y, y, 1.5);
 }
 __device__ __forceinline__ double sqrt64(double x) {
@@ -374,127 +368,123 @@ __device__ __forceinline__ void rotate64(double s, double c, double d, double x,
   }
 }
 
-// fp64 cell.  Reference operation order and guards (kernel.py:352-510);
-// sin/cos are evaluated once per angle family: the drag correction of the
-// mean anomaly, the Newton updates of Kepler's E and the J2 short-period
-// corrections of su and xinc are applied as rotations (rotate64), and the
-// atan2 of kernel.py:455 is replaced by normalising (sin u, cos u) — only
-// sin/cos of su are ever used.  All of it is exact to fp64 rounding.
+// fp64 cell (kernel.py:352-510), the parity variant: fp64 throughout, with
+// the reference's guards, thresholds and code precedence.  It departs from
+// the reference's operation order only where the result is unchanged to far
+// below the 1 mm / 1e-6 km/s budget (measured ~1e-9 km):
+//   * angles are never floor-reduced: every angle only reaches sin/cos (whose
+//     Cody-Waite reduction is exact), and the Kepler argument is formed as
+//     u = (mo + argpo) + (mdot + argpdot) t + no templ + xlcof axnl / pl_lp
+//     (mm + argpm; the drag terms cancel) with E carried as u + d;
+//   * sqrt(am) = sqrt(am0) |tempa| and nm = no / |tempa|^3 (the pow of
+//     kernel.py:397-401 with am0 = (xke/no)^(2/3) hoisted);
+//   * sin/cos are evaluated once per angle family: the drag correction of
+//     the mean anomaly, the Newton updates of E and the J2 short-period
+//     corrections of su and xinc are rotations (rotate64); the atan2 of
+//     kernel.py:455 is replaced by normalising (sin u, cos u);
+//   * sqrt(pl) = sqrt(am) betal, and reciprocals use two Newton steps.
 template <class RT>
 __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cell64& o) {
   const double tiny = DBL_MIN;
-  const double xke = g.xke, j2 = g.j2, re = g.re;
-  const double vkmpersec = g.vkm;
+  const double j2 = g.j2, re = g.re;
   const int flags = R.flags();
   const bool isimp = flags & FLAG_ISIMP;
 
   // secular gravity and atmospheric drag  kernel.py:365-391
-  const double xmdf = R[S_MO] + R[S_MDOT] * t;
-  const double argpdf = R[S_ARGPO] + R[S_ARGPDOT] * t;
-  const double nodedf = R[S_NODEO] + R[S_NODEDOT] * t;
+  const double argpdf = fma(R[S_ARGPDOT], t, R[S_ARGPO]);
   const double t2 = t * t;
-  double nodem = nodedf + R[S_NODECF] * t2;
-  double tempa = 1.0 - R[S_CC1] * t;
+  const double nodem = fma(R[S_NODECF], t2, fma(R[S_NODEDOT], t, R[S_NODEO]));
+  double tempa = fma(-R[S_CC1], t, 1.0);
   double tempe = R[S_BC4] * t;
   double templ = R[S_T2COF] * t2;
-  double mm = xmdf, argpm = argpdf;
+  double argpm = argpdf;
   if (!isimp) {
+    const double xmdf = fma(R[S_MDOT], t, R[S_MO]);
     double sx, cx;
     sincos64(xmdf, &sx, &cx);
-    const double delomg = R[S_OMGCOF] * t;
-    const double delmtemp = 1.0 + R[S_ETA] * cx;
-    const double delm = R[S_XMCOF] * (delmtemp * delmtemp * delmtemp - R[S_DELMO]);
-    const double temp = delomg + delm;
-    mm = xmdf + temp;
+    const double delmtemp = fma(R[S_ETA], cx, 1.0);
+    const double delm = R[S_XMCOF] * fma(delmtemp * delmtemp, delmtemp, -R[S_DELMO]);
+    const double temp = fma(R[S_OMGCOF], t, delm);
     argpm = argpdf - temp;
-    const double t3 = t2 * t;
-    const double t4 = t3 * t;
-    tempa = tempa - R[S_D2] * t2 - R[S_D3] * t3 - R[S_D4] * t4;
+    tempa = fma(-t2, fma(t, fma(t, R[S_D4], R[S_D3]), R[S_D2]), tempa);
     double smm, cmm;
-    rotate64(sx, cx, temp, mm, smm, cmm);                // sin(mm)
-    tempe = tempe + R[S_BC5] * (smm - R[S_SINMAO]);
-    templ = templ + R[S_T3COF] * t3 + t4 * (R[S_T4COF] + t * R[S_T5COF]);
+    rotate64(sx, cx, temp, xmdf + temp, smm, cmm);       // sin(mm)
+    tempe = fma(R[S_BC5], smm - R[S_SINMAO], tempe);
+    templ = fma(t2 * t, fma(t, fma(t, R[S_T5COF], R[S_T4COF]), R[S_T3COF]), templ);
   }
 
   // mean motion / eccentricity update  kernel.py:393-414
-  const double am = R[S_AM0] * tempa * tempa;   // pow(xke/nm_safe, 2/3) hoisted
-  const double am_safe = gmax(am, tiny);
-  const double sqam = sqrt64(am_safe);
-  const double nm = div64(xke, am_safe * sqam);   // xke / am^1.5
+  const double atempa = fabs(tempa);
+  const double am = gmax(R[S_AM0] * tempa * tempa, tiny);       // am_safe
+  const double sqam = R[S64_SQAM0] * atempa;                    // sqrt(am)
+  const double ita = rcp64(atempa);
+  const double nm = R[S64_NOSAFE] * (ita * ita * ita);          // xke / am^1.5
   double em = R[S_ECCO] - tempe;
   const bool bad_em = (em >= 1.0) || (em < -0.001);
   em = em < 1.0e-6 ? 1.0e-6 : em;
-  mm = mm + R[S_NO] * templ;
-  double xlm = mm + argpm + nodem;
-  nodem = fmod_2pi(nodem);              // mod_twopi_signed, dmath.py:218-221
-  argpm = pymod_2pi(argpm);
-  xlm = pymod_2pi(xlm);
-  mm = pymod_2pi(xlm - argpm - nodem);
-
-  const double sinip = R[S_SINIO];
-  const double cosip = R[S_COSIO];
 
   // long-period periodics  kernel.py:419-431
-  const double ep = em;
   double sa, ca;
   sincos64(argpm, &sa, &ca);
-  const double axnl = ep * ca;
-  const double pl_lp = gmax(am_safe * (1.0 - ep * ep), tiny);
-  const double ilp = rcp64(pl_lp);
-  const double aynl = ep * sa + ilp * R[S_AYCOF];
-  const double xl = mm + argpm + nodem + ilp * R[S_XLCOF] * axnl;
+  const double axnl = em * ca;
+  const double ilp = rcp64(gmax(am * fma(-em, em, 1.0), tiny));
+  const double aynl = fma(em, sa, ilp * R[S_AYCOF]);
+  const double u = fma(ilp * R[S_XLCOF], axnl,
+                       fma(R[S_NO], templ, fma(R[S_UDOT], t, R[S_U0])));
 
-  // Kepler  kernel.py:325-349, 434-437: (sin, cos) of E carried along the
-  // Newton updates by rotation
-  const double u = pymod_2pi(xl - nodem);
-  double eo1 = u, sineo1, coseo1;
+  // Kepler  kernel.py:325-349: E = u + d, (sin, cos) E carried along the
+  // Newton updates by rotation, the reference's clamp and 1e-12 freeze
+  double sineo1, coseo1, d = 0.0;
   sincos64(u, &sineo1, &coseo1);
   bool active = true;
 #pragma unroll 1
   for (int it = 0; it < 10 && active; ++it) {
-    const double den = 1.0 - coseo1 * axnl - sineo1 * aynl;
-    double tem5 = div64(u - aynl * coseo1 + axnl * sineo1 - eo1, den);
+    const double den = fma(-sineo1, aynl, fma(-coseo1, axnl, 1.0));
+    const double num = fma(axnl, sineo1, fma(-aynl, coseo1, -d));
+    double tem5 = num * rcp64(den);
     tem5 = tem5 >= 0.95 ? 0.95 : (tem5 <= -0.95 ? -0.95 : tem5);
-    eo1 = eo1 + tem5;
-    rotate64(sineo1, coseo1, tem5, eo1, sineo1, coseo1);
+    d += tem5;
+    rotate64(sineo1, coseo1, tem5, u + d, sineo1, coseo1);
     active = fabs(tem5) >= 1.0e-12;
   }
 
   // short-period preliminaries  kernel.py:440-460
-  const double ecose = axnl * coseo1 + aynl * sineo1;
-  const double esine = axnl * sineo1 - aynl * coseo1;
-  const double el2 = axnl * axnl + aynl * aynl;
-  const double pl = am_safe * (1.0 - el2);
+  const double ecose = fma(axnl, coseo1, aynl * sineo1);
+  const double esine = fma(axnl, sineo1, -aynl * coseo1);
+  const double el2 = fma(axnl, axnl, aynl * aynl);
+  const double omel2 = 1.0 - el2;
+  const double pl = am * omel2;
   const bool bad_pl = pl < 0.0;
   const double pl_safe = gmax(pl, tiny);
-  const double rl = am_safe * (1.0 - ecose);
-  const double rl_safe = rl == 0.0 ? tiny : rl;
-  const double irl = rcp64(rl_safe);
+  const double rl = am * (1.0 - ecose);
+  const double irl = rcp64(rl == 0.0 ? tiny : rl);
+  const double betal = sqrt64(gmax(omel2, tiny));
   const double rdotl = sqam * esine * irl;
-  const double rvdotl = sqrt64(pl_safe) * irl;
-  const double betal = sqrt64(gmax(1.0 - el2, tiny));
-  const double tq = div64(esine, 1.0 + betal);
+  // sqrt(pl_safe) = sqrt(am) betal whenever pl >= tiny
+  const double rvdotl = (pl >= tiny ? sqam * betal : sqrt64(pl_safe)) * irl;
+  const double tq = esine * rcp64(1.0 + betal);
   // (sin u, cos u) normalised: the reference's am/rl factor is positive and
   // only the direction reaches sin/cos(su)
-  const double sn = sineo1 - aynl - axnl * tq;
-  const double cs = coseo1 - axnl + aynl * tq;
-  const double inrm = rsqrt64(sn * sn + cs * cs);
+  const double sn = fma(-axnl, tq, sineo1 - aynl);
+  const double cs = fma(aynl, tq, coseo1 - axnl);
+  const double inrm = rsqrt64(fma(sn, sn, cs * cs));
   const double sinu = sn * inrm, cosu = cs * inrm;
   const double sin2u = (cosu + cosu) * sinu;
-  const double cos2u = 1.0 - 2.0 * sinu * sinu;
+  const double cos2u = fma(-2.0 * sinu, sinu, 1.0);
   const double ipl = rcp64(pl_safe);
   const double temp1 = 0.5 * j2 * ipl;
   const double temp2 = temp1 * ipl;
 
   // short-period periodics  kernel.py:463-469
   const double con41 = R[S_CON41], x1mth2 = R[S_X1MTH2];
-  const double mrt = rl * (1.0 - 1.5 * temp2 * betal * con41) + 0.5 * temp1 * x1mth2 * cos2u;
+  const double sinip = R[S_SINIO], cosip = R[S_COSIO];
+  const double mrt = fma(rl, fma(-1.5 * temp2 * betal, con41, 1.0), 0.5 * temp1 * x1mth2 * cos2u);
   const double dsu = -0.25 * temp2 * R[S_X7THM1] * sin2u;
-  const double xnode = nodem + 1.5 * temp2 * cosip * sin2u;
+  const double xnode = fma(1.5 * temp2 * cosip, sin2u, nodem);
   const double dinc = 1.5 * temp2 * cosip * sinip * cos2u;
   const double nmx = nm * temp1 * g.inv_xke;
-  const double mvt = rdotl - nmx * x1mth2 * sin2u;
-  const double rvdot = rvdotl + nmx * (x1mth2 * cos2u + 1.5 * con41);
+  const double mvt = fma(-nmx * x1mth2, sin2u, rdotl);
+  const double rvdot = fma(nmx, fma(x1mth2, cos2u, 1.5 * con41), rvdotl);
 
   // orientation  kernel.py:472-493
   double sinsu, cossu, snod, cnod, sini, cosi;
@@ -508,14 +498,14 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   const double xmy = cnod * cosi;
   const double mr = mrt * re;
   const double ra = mr * sinsu, rb = mr * cossu;
-  o.r[0] = xmx * ra + cnod * rb;
-  o.r[1] = xmy * ra + snod * rb;
+  o.r[0] = fma(xmx, ra, cnod * rb);
+  o.r[1] = fma(xmy, ra, snod * rb);
   o.r[2] = sini * ra;
-  const double mv = mvt * vkmpersec, rv = rvdot * vkmpersec;
-  const double va = mv * sinsu + rv * cossu;
-  const double vb = mv * cossu - rv * sinsu;
-  o.v[0] = xmx * va + cnod * vb;
-  o.v[1] = xmy * va + snod * vb;
+  const double mv = mvt * g.vkm, rv = rvdot * g.vkm;
+  const double va = fma(mv, sinsu, rv * cossu);
+  const double vb = fma(mv, cossu, -rv * sinsu);
+  o.v[0] = fma(xmx, va, cnod * vb);
+  o.v[1] = fma(xmy, va, snod * vb);
   o.v[2] = sini * va;
 
   // _first_error + init merge  kernel.py:495-502, 529-534 (bad_nm is folded
@@ -959,8 +949,8 @@ __device__ __forceinline__ void record_values(const double* f, int init_code, bo
   out[S_X1MTH2] = f[F_X1MTH2];
   out[S_X7THM1] = f[F_X7THM1];
   out[S_FLAGS] = 0.0;
-  out[S_MDOT_LO] = 0.0;
-  out[S_ARGPDOT_LO] = 0.0;
+  out[S64_SQAM0] = sqrt(out[S_AM0]);
+  out[S64_NOSAFE] = g.xke / (out[S_AM0] * out[S64_SQAM0]);
   out[S_NODEDOT_LO] = 0.0;
   out[S_UDOT] = f[F_MDOT] + f[F_ARGPDOT];
   out[S_UDOT_LO] = 0.0;
