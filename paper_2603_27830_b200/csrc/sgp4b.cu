@@ -436,9 +436,15 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   // Newton updates by rotation, the reference's clamp and 1e-12 freeze
   double sineo1, coseo1, d = 0.0;
   sincos64(u, &sineo1, &coseo1);
+  // Newton from E0 = u: |E - E_k| <~ (e/2)^(2^k - 1) e^(2^k), so for the
+  // fp32 classes e < 0.004 and e < 0.1 (flags) two and three steps land
+  // below 1e-17 rad, where the reference's extra step only confirms the
+  // 1e-12 freeze; other orbits run the reference loop
+  const int kfix = (flags >> KEPLER_SHIFT) & 0xf;
+  const int kmax = kfix == 1 ? 2 : kfix == 2 ? 3 : 10;
   bool active = true;
 #pragma unroll 1
-  for (int it = 0; it < 10 && active; ++it) {
+  for (int it = 0; it < kmax && active; ++it) {
     const double den = fma(-sineo1, aynl, fma(-coseo1, axnl, 1.0));
     const double num = fma(axnl, sineo1, fma(-aynl, coseo1, -d));
     double tem5 = num * rcp64(den);
