@@ -58,6 +58,20 @@ def test_vectorised_columns_equal_record_route(all_pairs, ref_parse):
         assert np.array_equal(cols[i], ref_parse["el_" + f]), f
 
 
+@pytest.mark.parametrize("field", [" 12345-3", "-11606-4", " 00000-0", " 00000+0", " 12345+1",
+                                   "+12345-9", " 1-5", "-9+9", "      ", " 12345", "-00001-1",
+                                   " 99999-9"])
+def test_implied_exponent_columns_match_scalar(field):
+    """The vectorised B* decoder (every shape the scalar decoder accepts)
+    equals _implied_exponent bit for bit (tle.py:_implied_exponent)."""
+    from paper_2603_27830_b200.tle import _implied_exponent, _implied_exponent_columns
+    raw = np.char.strip(np.array([field, " 12345-3", field], dtype="S8"))
+    got = _implied_exponent_columns(raw)
+    want = _implied_exponent(field, "bstar")
+    assert got[0] == want and got[2] == want and got[1] == _implied_exponent(" 12345-3", "b")
+    assert np.signbit(got[0]) == np.signbit(want)
+
+
 def test_checksum_rules(real_records):
     l1, _ = real_records["ISS"]
     assert checksum(l1) == int(l1[68])
