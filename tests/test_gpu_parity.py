@@ -420,3 +420,40 @@ def test_device_result_views_and_gather(corpus_columns):
     assert (lo, hi) == shard_bounds(9, 1, 0) == (0, 9)
     p, e = gather_grid(local.planes, local.error, 9)
     assert torch.equal(p, local.planes) and torch.equal(e, local.error)
+
+
+def test_fp32_kepler_classes_and_drag(oracle, corpus_columns):
+    """The fp32 cell specialises on the satellite's Kepler class (e < 0.003:
+    series for 1/den, betal, 1/(1+betal), 1/pl; e < 0.1; e < 0.4; other) and
+    on isimp.  Sweep eccentricity across every class boundary and B* over
+    three decades for two weeks: codes must equal the reference fp64 codes,
+    and the fp32 error against reference fp64 must stay within the
+    reference's own fp32 error on the same cells (+50 m)."""
+    pkg = _gpu()
+    eccs = [1e-5, 1e-4, 0.0029, 0.0031, 0.02, 0.099, 0.101, 0.3, 0.41, 0.6]
+    bstars = [1e-5, 3e-4, 5e-3]
+    base = corpus_columns[:, :2]          # one regular, one low-perigee-ish LEO
+    cols = []
+    for e in eccs:
+        for b in bstars:
+            for k in range(base.shape[1]):
+                c = base[:, k].copy()
+                c[1] = e
+                c[6] = b
+                cols.append(c)
+    cols = np.array(cols).T
+    times = np.arange(0.0, 20160.0, 97.0)
+    ref64, codes64 = oracle.grid(oracle.init_columns(cols, 64), times, workers=4)
+    ref32, _ = oracle.grid(oracle.init_columns(cols, 32), times, workers=4)
+    res = pkg.propagate_batch(pkg.init_batch(cols, precision=32), times)
+    assert np.array_equal(res.error, codes64)
+    ok = codes64 == 0
+    dr, _ = _diff(res.planes, ref64, ok)
+    dr_ref, _ = _diff(ref32, ref64, ok)
+    print(f"\nfp32 class sweep ({cols.shape[1]} sats x {times.size}): max|dr| {dr.max() * 1e3:.1f} m "
+          f"(reference fp32 {dr_ref.max() * 1e3:.1f} m), ok cells {int(ok.sum())}")
+    assert dr.max() <= dr_ref.max() + 0.05 and dr.max() < 0.5
+    res64 = pkg.propagate_batch(pkg.init_batch(cols, precision=64), times)
+    assert np.array_equal(res64.error, codes64)
+    dr64, dv64 = _diff(res64.planes, ref64, ok)
+    assert dr64.max() <= TOL64_R and dv64.max() <= TOL64_V
