@@ -36,7 +36,10 @@
 
 #include "../../include/sgp4b.h"
 
-// build-time tuning knobs (defaults are the shipped configuration)
+// build-time tuning knobs (defaults are the shipped configuration; the
+// alternatives measured slower, DESIGN.md §5/§8).  Analysis-only builds:
+// SGP4B_NOSTORE (compute without the output stores) and
+// SGP4B_ONLY_CLASS_K1 (one class instance, for tools/sass_mix.sh).
 #ifndef SGP4B_SMEM_REC
 #define SGP4B_SMEM_REC 0          // fp32 records in shared memory (default: registers)
 #endif
