@@ -54,9 +54,9 @@
 #endif
 constexpr int kF64Unroll = SGP4B_F64_UNROLL;   // fp64 cells interleaved per lane
 #ifndef SGP4B_MINB64
-#define SGP4B_MINB64 2
+#define SGP4B_MINB64 1
 #endif
-constexpr int kGridMinBlocks64 = SGP4B_MINB64; // resident 256-thread blocks per SM (fp64)
+constexpr int kGridMinBlocks64 = SGP4B_MINB64; // resident blocks per SM (fp64)
 
 namespace {
 
@@ -1230,15 +1230,15 @@ __global__ void pack_kernel(const double* __restrict__ satrec, const int32_t* __
 #define SGP4B_CELLS 4
 #endif
 #ifndef SGP4B_MINB
-#define SGP4B_MINB 2
+#define SGP4B_MINB 1
 #endif
 constexpr int kCellsPerLane = SGP4B_CELLS;          // consecutive time steps per lane
 constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // one work item (chunk)
 #ifndef SGP4B_BLOCK
-#define SGP4B_BLOCK 256
+#define SGP4B_BLOCK 512     // one 16-warp block per SM: its warps own adjacent rows
 #endif
 constexpr int kGridBlock = SGP4B_BLOCK;
-constexpr int kGridMinBlocks = SGP4B_MINB;   // resident 256-thread blocks per SM (fp32)
+constexpr int kGridMinBlocks = SGP4B_MINB;   // resident blocks per SM (fp32)
 
 __device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
 __device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
