@@ -1511,6 +1511,12 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
 // compiler made.  The Python layer pads unaligned grids so every public call
 // runs this instance; VEC = false only serves raw C-ABI callers with
 // unaligned strides.
+#ifdef SGP4B_TIMELINE
+// analysis build: per-warp (start, first row done, end, smid) in ns
+constexpr int kTimelineWarps = 1 << 16;
+__device__ unsigned long long g_timeline[kTimelineWarps][4];
+#endif
+
 template <typename T, bool VEC, bool LO>
 __global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : kGridMinBlocks64)
 grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t n,
@@ -1538,6 +1544,11 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
     const int64_t jf = (g0 - s0 * chunks) * kCellsPerWarp + lane * kCellsPerLane;
     if (jf < m) asm volatile("prefetch.global.L1 [%0];" ::"l"(times + s0 * times_ld + jf));
   }
+#ifdef SGP4B_TIMELINE
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  bool first_row = true;
+#endif
   for (int64_t gi = g0; gi < g1;) {
     const int64_t sat = gi / chunks;
     const int64_t c0 = gi - sat * chunks;
@@ -1561,7 +1572,26 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
                      LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
                      plane_stride, codes + sat * code_stride);
     gi += c1 - c0;
+#ifdef SGP4B_TIMELINE
+    if (first_row && lane == 0 && w < kTimelineWarps) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_timeline[w][1] = t;
+    }
+    first_row = false;
+#endif
   }
+#ifdef SGP4B_TIMELINE
+  if (lane == 0 && w < kTimelineWarps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_timeline[w][0] = t_start;
+    g_timeline[w][2] = t;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_timeline[w][3] = smid;
+  }
+#endif
 }
 
 template <typename T>
@@ -1676,6 +1706,13 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 extern "C" {
 
 int sgp4b_abi_version(void) { return 1; }
+
+#ifdef SGP4B_TIMELINE
+int sgp4b_debug_timeline(unsigned long long* host, int warps) {
+  if (warps > kTimelineWarps) warps = kTimelineWarps;
+  return (int)cudaMemcpyFromSymbol(host, g_timeline, sizeof(unsigned long long) * 4 * warps);
+}
+#endif
 
 const char* sgp4b_last_error(void) { return g_last_error; }
 
