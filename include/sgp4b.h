@@ -41,7 +41,12 @@ extern "C" {
 #define SGP4B_RECORD_SLOTS 40
 
 /* grav: HOST pointer to 8 doubles {mu, radius_earth_km, xke, tumin, j2, j3,
- * j4, j3oj2} (gravity.py:13-28); read at launch time. */
+ * j4, j3oj2} (gravity.py:13-28); read at launch time.  The propagate calls
+ * must pass the model the records were built with (init/pack): as in the
+ * reference, where SatInit carries its grav (kernel.py:64) and _propagate
+ * reads init.grav (kernel.py:353), the model belongs to the satrec, and the
+ * fp32 records fold 0.5 j2, the Earth radius and the km/s scale into their
+ * per-satellite coefficients. */
 
 /* Initialisation, one thread per satellite, always evaluated in fp64.
  * Replaces _sgp4_init (kernel.py:154-322) incl. the epoch evaluation
