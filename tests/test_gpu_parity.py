@@ -425,13 +425,13 @@ def test_device_result_views_and_gather(corpus_columns):
 def test_fp32_kepler_classes_and_drag(oracle, corpus_columns):
     """The fp32 cell specialises on the satellite's Kepler class (e < 0.003:
     series for 1/den, betal, 1/(1+betal), 1/pl; e < 0.1; e < 0.4; other) and
-    on isimp.  Sweep eccentricity across every class boundary and B* over
+    on isimp.  Sweep eccentricity across every class boundary and B* (either sign) over
     three decades for two weeks: codes must equal the reference fp64 codes,
     and the fp32 error against reference fp64 must stay within the
     reference's own fp32 error on the same cells (+50 m)."""
     pkg = _gpu()
     eccs = [1e-5, 1e-4, 0.0029, 0.0031, 0.02, 0.099, 0.101, 0.3, 0.41, 0.6]
-    bstars = [1e-5, 3e-4, 5e-3]
+    bstars = [1e-5, 3e-4, 5e-3, -3e-4, -5e-3]
     base = corpus_columns[:, :2]          # one regular, one low-perigee-ish LEO
     cols = []
     for e in eccs:
