@@ -66,34 +66,75 @@ def _peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while work runs."""
+    """SM clock + throttle reasons sampled while the timed region runs.
 
+    NVML is polled every ~2 ms from a thread (nvidia-smi's 100 ms loop would
+    see a few-ms timed region once at best); ``region(True/False)`` brackets
+    the timed launches and the summary covers the samples taken inside it.
+    Falls back to ``nvidia-smi -lms 100`` when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+                ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+                ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples: list[tuple[float, int, bool]] = []    # (sm MHz, reason bits, in region)
+        self.in_region = False
+        self.stop = threading.Event()
+        self.nvml = None
         self.proc = None
         self.lines: list[str] = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._poll, daemon=True)
             self._t.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self._t = threading.Thread(target=self._read, daemon=True)
+                self._t.start()
+            except (OSError, FileNotFoundError):
+                self.proc = None
         return self
+
+    def region(self, inside: bool) -> None:
+        self.in_region = inside
+
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                bits = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle))
+                self.samples.append((mhz, bits, self.in_region))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml is not None:
+            self._t.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -102,6 +143,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
+        if self.nvml is not None:
+            inside = [x for x in self.samples if x[2]]
+            use = inside or self.samples
+            if not use:
+                return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+            reasons = sorted({name for _, bits, _ in use for name, attr in self.REASONS
+                              if bits & int(getattr(self.nvml, attr, 0))})
+            return {"sm_mhz": statistics.median(x[0] for x in use), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(use),
+                    "source": "nvml, 2 ms polling, " + ("timed region" if inside else "whole run")}
         rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -117,7 +168,7 @@ class ClockSampler:
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({names[i] for r in busy for i, v in enumerate(r[3]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in busy), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(busy)}
+                "reasons": reasons, "samples": len(busy), "source": "nvidia-smi -lms 100"}
 
 
 def time_task_cpu(task, min_trial_s: float = 0.2, trials: int = 5) -> float:
@@ -278,6 +329,7 @@ def run_ours(args, world, rank, local) -> None:
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     region0 = torch.cuda.Event(enable_timing=True)
     region1 = torch.cuda.Event(enable_timing=True)
+    sampler.region(True)
     region0.record(stream)
     for k in range(args.steps):
         flush_l2(k)                             # L2 flush, outside the kernel's events
@@ -286,6 +338,7 @@ def run_ours(args, world, rank, local) -> None:
         ends[k].record(stream)
     region1.record(stream)
     torch.cuda.synchronize()
+    sampler.region(False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -297,6 +350,31 @@ def run_ours(args, world, rank, local) -> None:
     total_ms_max = float(t.item())
     ms_per_step = total_ms_max / args.steps
     value = cells * world / (ms_per_step * 1e-3)
+
+    # ---- paper convention: init + propagate, element
+    # columns resident in HBM, same flush + event protocol -----------------
+    from paper_2603_27830_b200.gravity import WGS72
+    el_dev = torch.from_numpy(np.ascontiguousarray(cols, dtype=np.float64)).to(device)
+
+    def init_and_launch():
+        d = _device.init_device_tensor(el_dev, WGS72, precision, device)
+        _device.propagate_grid(d, t_dev, planes, error)
+
+    ip_ms = []
+    for k in range(max(3, min(args.steps, 10)) + 2):
+        flush_l2(k)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        init_and_launch()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ip_ms.append(a.elapsed_time(b))
+    ip = torch.tensor([statistics.median(ip_ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(ip, op=dist.ReduceOp.MAX)
+    init_prop_ms = float(ip.item())
 
     # ---- e2e: public API with host buffers --------------------------------
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -326,8 +404,7 @@ def run_ours(args, world, rank, local) -> None:
         bpc = BYTES_PER_CELL[precision]
         achieved_gbs = cells * bpc / (ms_per_step * 1e-3) / 1e9
         traffic = _traffic(args.workload, precision)
-        lanes = 128 if precision == 32 else 64
-        flop_peak = 148 * lanes * 2 * peaks["sm_max_mhz"] * 1e6
+        flop_peak, flop_src = _flop_peak(precision, peaks)
         t_hbm = cells * bpc / (peaks["hbm_gbs"] * 1e9)
         t_flop = cells * FLOPS_PER_CELL / flop_peak
         line = {
@@ -352,7 +429,7 @@ def run_ours(args, world, rank, local) -> None:
                 "algorithmic_bytes_per_cell": bpc,
                 "t_hbm_us": t_hbm * 1e6, "t_flop_us": t_flop * 1e6,
                 "flops_per_cell": FLOPS_PER_CELL,
-                "flop_peak_tflops_derived": flop_peak / 1e12,
+                "flop_peak_tflops": flop_peak / 1e12, "flop_peak_source": flop_src,
                 "frac_of_roofline": max(t_hbm, t_flop) / (ms_per_step * 1e-3),
             },
             "e2e": {"value": cells * world / e2e_s, "unit": UNIT,
@@ -360,6 +437,10 @@ def run_ours(args, world, rank, local) -> None:
                     "h2d_bytes_per_step": 7 * n * 8 + m * (4 if precision == 32 else 8),
                     "d2h_bytes_per_step": cells * bpc,
                     "api": "propagate_batch(init_batch(host columns), host times) -> pinned numpy"},
+            "init_plus_propagate": {"ms_per_step": init_prop_ms,
+                                    "value": cells * world / (init_prop_ms * 1e-3),
+                                    "note": "paper convention (PAPER.md:67-71): init kernel + "
+                                            "grid kernel, element columns in HBM, L2 flushed"},
             "gpu_launches": args.steps,
             "clocks": clocks,
             "kernel_ms_min": min(kernel_ms), "kernel_ms_median": statistics.median(kernel_ms),
@@ -378,6 +459,19 @@ def _device_alloc(n, m, precision, device):
             torch.empty((n, m), dtype=torch.int32, device=device))
 
 
+def _flop_peak(precision: int, peaks: dict):
+    """FP32/FP64 FMA peak: the FMA microbenchmark (profiles/r01_pipes.json,
+    tools/exp/pipes.py) when present, else 148 SM x lanes x 2 x max clock."""
+    path = ROOT / "profiles" / "r01_pipes.json"
+    key = "fp32_ffma2_tflops" if precision == 32 else "fp64_dfma_tflops"
+    if path.exists():
+        d = json.loads(path.read_text())
+        if key in d:
+            return float(d[key]) * 1e12, "measured (profiles/r01_pipes.json)"
+    lanes = 128 if precision == 32 else 64
+    return 148 * lanes * 2 * peaks["sm_max_mhz"] * 1e6, "derived (148 SM x lanes x 2 x max clock)"
+
+
 def _traffic(workload: str, precision: int):
     """dram read+write bytes per launch from the committed ncu --set full
     capture (profiles/ncu_traffic.json), or None."""
@@ -391,7 +485,7 @@ def _traffic(workload: str, precision: int):
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c2")
