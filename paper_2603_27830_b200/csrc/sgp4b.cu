@@ -36,6 +36,9 @@
 
 #include "../../include/sgp4b.h"
 
+// helpers used only by the non-default build knobs below
+#pragma nv_diag_suppress 177
+
 // build-time tuning knobs (defaults are the shipped configuration; the
 // alternatives measured slower, DESIGN.md §5/§8).  Analysis-only builds:
 // SGP4B_NOSTORE (compute without the output stores) and
@@ -914,11 +917,29 @@ __device__ __forceinline__ void split_df(double x, float& hi, float& lo) {
 }
 
 template <typename T>
-__device__ __forceinline__ void store_record(const double* f, int init_code, bool isimp,
-                                             const Grav& g, T* __restrict__ rec);
+__device__ __forceinline__ void store_record(const double* f, const double* v, int flags,
+                                             bool isimp, const Grav& g, T* __restrict__ rec);
 
-__device__ __forceinline__ void record_values(const double* f, int init_code, bool isimp,
-                                              const Grav& g, double* out, int& flags) {
+// (xke / n)^(2/3) as cbrt squared: within 2 ulp of pow(x, 2/3) (the
+// reference's np.power), at a fraction of the libdevice pow chain
+__device__ __forceinline__ double pow2o3(double x) {
+  const double c = cbrt(x);
+  return c * c;
+}
+
+// flags word of a record: isimp, Kepler class, persistent init code
+__device__ __forceinline__ int record_flags(const double* f, int init_code, bool isimp) {
+  const bool bad_nm = f[F_NO_UNKOZAI] <= 0.0;
+  // kernel.py:532: init codes persist except 6; bad_nm (per satellite) is
+  // folded in behind them, preserving _first_error precedence 2 > 1 > 4 > 6
+  int persistent = init_code == 6 ? 0 : init_code;
+  if (persistent == 0 && bad_nm) persistent = 2;
+  return (isimp ? FLAG_ISIMP : 0) | (bad_nm ? FLAG_BAD_NM : 0) |
+         (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0xff) << CODE_SHIFT);
+}
+
+// fp64 record values (flags slot left 0; see record_flags)
+__device__ __forceinline__ void record_values(const double* f, const Grav& g, double* out) {
   const double no = f[F_NO_UNKOZAI];
   const bool bad_nm = no <= 0.0;
   const double nm_safe = bad_nm ? 1.0e-4 : no;
@@ -945,7 +966,7 @@ __device__ __forceinline__ void record_values(const double* f, int init_code, bo
   out[S_T4COF] = f[F_T4COF];
   out[S_T5COF] = f[F_T5COF];
   out[S_NO] = no;
-  out[S_AM0] = pow(g.xke / nm_safe, kX2o3);
+  out[S_AM0] = pow2o3(g.xke / nm_safe);
   out[S_ECCO] = f[F_ECCO];
   out[S_INCLO] = f[F_INCLO];
   double si, ci;
@@ -964,23 +985,15 @@ __device__ __forceinline__ void record_values(const double* f, int init_code, bo
   out[S_UDOT] = f[F_MDOT] + f[F_ARGPDOT];
   out[S_UDOT_LO] = 0.0;
   out[S_U0] = pymod_2pi(f[F_MO] + f[F_ARGPO]);
-  // kernel.py:532: init codes persist except 6; bad_nm (per satellite) is
-  // folded in behind them, preserving _first_error precedence 2 > 1 > 4 > 6
-  int persistent = init_code == 6 ? 0 : init_code;
-  if (persistent == 0 && bad_nm) persistent = 2;
-  flags = (isimp ? FLAG_ISIMP : 0) | (bad_nm ? FLAG_BAD_NM : 0) |
-          (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0xff) << CODE_SHIFT);
 }
 
 template <>
-__device__ __forceinline__ void store_record<double>(const double* f, int init_code, bool isimp,
-                                                     const Grav& g, double* __restrict__ rec) {
-  double v[S_COUNT];
-  int flags;
-  record_values(f, init_code, isimp, g, v, flags);
-  v[S_FLAGS] = __longlong_as_double((long long)flags);
+__device__ __forceinline__ void store_record<double>(const double* f, const double* v, int flags,
+                                                     bool isimp, const Grav& g,
+                                                     double* __restrict__ rec) {
 #pragma unroll
   for (int i = 0; i < S_COUNT; ++i) rec[i] = v[i];
+  rec[S_FLAGS] = __longlong_as_double((long long)flags);
 }
 
 // reduce an angle to [-pi, pi): fp32 has the most resolution there
@@ -990,11 +1003,9 @@ __device__ __forceinline__ double signed_2pi(double x) {
 }
 
 template <>
-__device__ __forceinline__ void store_record<float>(const double* f, int init_code, bool isimp,
-                                                    const Grav& g, float* __restrict__ rec) {
-  double v[S_COUNT];
-  int flags;
-  record_values(f, init_code, isimp, g, v, flags);
+__device__ __forceinline__ void store_record<float>(const double* f, const double* v, int flags,
+                                                    bool isimp, const Grav& g,
+                                                    float* __restrict__ rec) {
   double o[S_COUNT];
 #pragma unroll
   for (int i = 0; i < S_COUNT; ++i) o[i] = 0.0;
@@ -1052,7 +1063,8 @@ __device__ __forceinline__ void store_record<float>(const double* f, int init_co
 // ======================================================================
 // Init (kernel.py:154-322), fp64, one thread per satellite
 // ======================================================================
-__device__ void init_one(const double el[7], const Grav& g, double* f, int& code, bool& isimp_out) {
+__device__ void init_one(const double el[7], const Grav& g, double* f, double* v, int& code,
+                         bool& isimp_out) {
   const double tiny = DBL_MIN;
   const double xke = g.xke, j2 = g.j2, j3oj2 = g.j3oj2, j4 = g.j4, re = g.re;
   const double no_kozai = el[0], ecco = el[1], inclo = el[2], nodeo = el[3];
@@ -1069,7 +1081,7 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, int& code
   const double cosio2 = cosio * cosio;
 
   // un-Kozai  :187-193
-  const double ak = pow(xke / no_safe, kX2o3);
+  const double ak = pow2o3(xke / no_safe);
   const double d1 = 0.75 * j2 * (3.0 * cosio2 - 1.0) / (rteosq * omeosq);
   double del = d1 / (ak * ak);
   const double adel = ak * (1.0 - del * del - del * (1.0 / 3.0 + 134.0 * del * del / 81.0));
@@ -1077,7 +1089,7 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, int& code
   const double no_unkozai = no_safe / (1.0 + del);
   const bool deep_space = kTwoPi / no_unkozai >= 225.0;             // :195
 
-  const double ao = pow(xke / no_unkozai, kX2o3);
+  const double ao = pow2o3(xke / no_unkozai);
   const double sinio = sin(inclo);
   const double po = ao * omeosq;
   const double con42 = 1.0 - 5.0 * cosio2;
@@ -1089,11 +1101,13 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, int& code
 
   // s* and (q0-s)^4 by perigee  :209-221
   const double ss = 78.0 / re + 1.0;
-  const double qzms2t = pow((120.0 - 78.0) / re, 4.0);
+  const double q2 = (120.0 - 78.0) / re;
+  const double qzms2t = (q2 * q2) * (q2 * q2);
   const bool low_perige = perige < 156.0;
   const double sfour_low = perige < 98.0 ? 20.0 : perige - 78.0;
   const double qzms24temp = (120.0 - sfour_low) / re;
-  const double qzms24 = low_perige ? pow(qzms24temp, 4.0) : qzms2t;
+  const double qz2 = qzms24temp * qzms24temp;
+  const double qzms24 = low_perige ? qz2 * qz2 : qzms2t;
   const double sfour = low_perige ? sfour_low / re + 1.0 : ss;
 
   // drag coefficients and secular rates  :223-275
@@ -1105,8 +1119,9 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, int& code
   const double etasq = eta * eta;
   const double eeta = ecco * eta;
   const double psisq = gmax(fabs(1.0 - etasq), tiny);
-  const double coef = qzms24 * pow(tsi, 4.0);
-  const double coef1 = coef / pow(psisq, 3.5);
+  const double tsi2 = tsi * tsi;
+  const double coef = qzms24 * (tsi2 * tsi2);
+  const double coef1 = coef / (psisq * psisq * psisq * sqrt(psisq));      // psisq^3.5
   const double cc2 = coef1 * no_unkozai *
       (ao * (1.0 + 1.5 * etasq + eeta * (4.0 + etasq)) +
        0.375 * j2 * tsi / psisq * con41 * (8.0 + 3.0 * etasq * (8.0 + etasq)));
@@ -1177,9 +1192,10 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, int& code
 
   // epoch evaluation  :316-322
   Rec<double> R;
-  int flags;
-  record_values(f, 0, isimp, g, R.v, flags);
-  R.v[S_FLAGS] = __longlong_as_double((long long)flags);
+  record_values(f, g, R.v);
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) v[i] = R.v[i];
+  R.v[S_FLAGS] = __longlong_as_double((long long)record_flags(f, 0, isimp));
   Cell64 c0;
   cell64(R, 0.0, g, c0);
   if (code == 0) code = c0.code;
@@ -1193,19 +1209,20 @@ __global__ void init_kernel(const double* __restrict__ el, int64_t n, Grav g,
   double e[7];
 #pragma unroll
   for (int k = 0; k < 7; ++k) e[k] = el[k * n + i];
-  double f[F_COUNT];
+  double f[F_COUNT], v[S_COUNT];
   int code;
   bool simp;
-  init_one(e, g, f, code, simp);
+  init_one(e, g, f, v, code, simp);
 #pragma unroll
   for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
   codes[i] = code;
   isimp[i] = simp ? 1 : 0;
   if (rec != nullptr) {
+    const int flags = record_flags(f, code, simp);
     if (precision == 64)
-      store_record<double>(f, code, simp, g, static_cast<double*>(rec) + i * S_COUNT);
+      store_record<double>(f, v, flags, simp, g, static_cast<double*>(rec) + i * S_COUNT);
     else
-      store_record<float>(f, code, simp, g, static_cast<float*>(rec) + i * S_COUNT);
+      store_record<float>(f, v, flags, simp, g, static_cast<float*>(rec) + i * S_COUNT);
   }
 }
 
@@ -1217,10 +1234,14 @@ __global__ void pack_kernel(const double* __restrict__ satrec, const int32_t* __
   double f[F_COUNT];
 #pragma unroll
   for (int k = 0; k < F_COUNT; ++k) f[k] = satrec[k * n + i];
+  double v[S_COUNT];
+  record_values(f, g, v);
+  const bool simp = isimp[i] != 0;
+  const int flags = record_flags(f, codes[i], simp);
   if (precision == 64)
-    store_record<double>(f, codes[i], isimp[i] != 0, g, static_cast<double*>(rec) + i * S_COUNT);
+    store_record<double>(f, v, flags, simp, g, static_cast<double*>(rec) + i * S_COUNT);
   else
-    store_record<float>(f, codes[i], isimp[i] != 0, g, static_cast<float*>(rec) + i * S_COUNT);
+    store_record<float>(f, v, flags, simp, g, static_cast<float*>(rec) + i * S_COUNT);
 }
 
 // ======================================================================
