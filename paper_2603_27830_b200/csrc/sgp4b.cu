@@ -130,8 +130,8 @@ enum Slot32 {
   P_SINIO, P_COSIO,
   P_COUNT
 };
-static_assert(P_FLAGS == S_FLAGS, "fp32 flags slot");
-static_assert(P_COUNT <= S_COUNT, "fp32 record fits the packed slot count");
+static_assert((int)P_FLAGS == (int)S_FLAGS, "fp32 flags slot");
+static_assert((int)P_COUNT <= (int)S_COUNT, "fp32 record fits the packed slot count");
 
 // flags word
 constexpr int FLAG_ISIMP = 1;
