@@ -363,7 +363,15 @@ __device__ __forceinline__ double sqrt64(double x) {
 // otherwise a direct sincos of the new angle `x`.
 __device__ __forceinline__ void rotate64(double s, double c, double d, double x, double& so,
                                          double& co) {
-  if (fabs(d) < 0.015625) {
+  if (fabs(d) < 0.0009765625) {
+    // |d| < 2^-10: sin d = d - d^3/6, cos d = 1 - d^2/2 + d^4/24 (truncation
+    // d^5/120 < 8e-18, below fp64 resolution of the result)
+    const double d2 = d * d;
+    const double sd = fma(d * d2, -1.0 / 6.0, d);
+    const double cd = fma(d2, fma(d2, 1.0 / 24.0, -0.5), 1.0);
+    so = fma(s, cd, c * sd);
+    co = fma(c, cd, -s * sd);
+  } else if (fabs(d) < 0.015625) {
     const double d2 = d * d;
     const double sd = d * fma(d2, fma(d2, fma(d2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
     const double cd = fma(d2, fma(d2, fma(d2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
