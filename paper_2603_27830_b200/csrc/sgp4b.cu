@@ -1353,27 +1353,6 @@ __device__ __forceinline__ void compute_n(const RT& R, const float (&th)[kCellsP
   }
 }
 
-// warp-uniform dispatch on the satellite's (isimp, Kepler count)
-template <bool LO, class RT>
-__device__ __forceinline__ void compute_cells(const RT& R, const float (&th)[kCellsPerLane],
-                                              const float (&tl)[kCellsPerLane], const Grav& g,
-                                              float (&out)[6][kCellsPerLane],
-                                              int (&code)[kCellsPerLane]) {
-  const int flags = R.flags();
-  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
-  if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) compute_n<false, 1, LO>(R, th, tl, g, out, code);
-    else if (kit == 2) compute_n<false, 2, LO>(R, th, tl, g, out, code);
-    else if (kit == 3) compute_n<false, 3, LO>(R, th, tl, g, out, code);
-    else compute_n<false, 0, LO>(R, th, tl, g, out, code);
-  } else {
-    if (kit == 1) compute_n<true, 1, LO>(R, th, tl, g, out, code);
-    else if (kit == 2) compute_n<true, 2, LO>(R, th, tl, g, out, code);
-    else if (kit == 3) compute_n<true, 3, LO>(R, th, tl, g, out, code);
-    else compute_n<true, 0, LO>(R, th, tl, g, out, code);
-  }
-}
-
 template <bool LO, class RT>
 __device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kCellsPerLane],
                                               const float (&)[kCellsPerLane], const Grav& g,
