@@ -236,7 +236,10 @@ def run_reference(args, world, rank) -> None:
     desc, nsat, tfn, default_prec = WORKLOADS[args.workload]
     precision = args.precision or default_prec
     times = tfn()
-    rows = min(nsat, args.ref_rows)
+    # bounded sample: ~2e9 cells over the whole --steps/--warmup run (about a
+    # minute on 16 host threads), at most the workload's own catalogue
+    budget_rows = int(2.0e9 / max(1, args.steps + args.warmup) / times.size)
+    rows = max(16, min(nsat, args.ref_rows, budget_rows))
     cols = starlink_like(rows)
     workers = oracle.default_workers()
 
