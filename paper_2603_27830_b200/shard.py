@@ -25,6 +25,16 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def shard_plan(n: int, m: int, world: int, rank: int) -> tuple[str, int, int]:
+    """What ``rank`` propagates: ``("rows", lo, hi)`` — a satellite range —
+    normally, or ``("cols", lo, hi)`` — all satellites over a time range —
+    when there are fewer satellites than ranks (e.g. C1, one ISS record),
+    so no GPU idles."""
+    if n >= world or m < world:
+        return ("rows",) + shard_bounds(n, world, rank)
+    return ("cols",) + shard_bounds(m, world, rank)
+
+
 def world_info(group=None) -> tuple[int, int]:
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(group), dist.get_rank(group)
@@ -43,29 +53,43 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
 
 def propagate_sharded(columns: np.ndarray, times, precision: int = 32, group=None,
                       device=None):
-    """Rank-local init + propagate of this rank's satellite shard.
+    """Rank-local init + propagate of this rank's shard (``shard_plan``).
 
     ``columns`` is the full (7, n) catalogue (every rank may hold it; it is
-    56 B per satellite).  Returns (BatchResult of device tensors, (lo, hi)).
+    56 B per satellite).  Returns (BatchResult of device tensors or None,
+    (axis, lo, hi)).
     """
     from .batch import init_batch, propagate_batch_device
 
     world, rank = world_info(group)
-    lo, hi = shard_bounds(columns.shape[1], world, rank)
+    times = np.asarray(times)
+    axis, lo, hi = shard_plan(columns.shape[1], times.shape[0], world, rank)
     if hi <= lo:
-        return None, (lo, hi)
-    sats = init_batch(columns[:, lo:hi], precision=precision, device=device)
-    return propagate_batch_device(sats, times), (lo, hi)
+        return None, (axis, lo, hi)
+    if axis == "rows":
+        sats = init_batch(columns[:, lo:hi], precision=precision, device=device)
+        return propagate_batch_device(sats, times), (axis, lo, hi)
+    sats = init_batch(columns, precision=precision, device=device)
+    return propagate_batch_device(sats, times[lo:hi]), (axis, lo, hi)
 
 
 def gather_grid(planes: torch.Tensor, error: torch.Tensor, n_total: int, group=None,
-                dst: int = 0):
+                dst: int = 0, axis: str = "rows", m_total: int | None = None):
     """Assemble the full (6, N, M) / (N, M) grid on rank ``dst`` from the
-    per-rank row shards (shards follow shard_bounds).  Returns the tensors on
-    ``dst`` and None elsewhere.  Works with gloo (CPU tensors) and NCCL."""
+    per-rank shards: row shards (``axis="rows"``, bounds from shard_bounds
+    over ``n_total``) or time-column shards (``axis="cols"``, bounds over
+    ``m_total``).  Returns the tensors on ``dst`` and None elsewhere.  Works
+    with gloo (CPU tensors) and NCCL."""
     world, rank = world_info(group)
     if world == 1:
         return planes, error
+    if axis == "cols":
+        # transpose to row form, reuse the row path, transpose back
+        got = gather_grid(planes.transpose(1, 2).contiguous(), error.t().contiguous(),
+                          int(m_total), group=group, dst=dst)
+        if got is None:
+            return None
+        return got[0].transpose(1, 2).contiguous(), got[1].t().contiguous()
     m = planes.shape[2]
     bounds = [shard_bounds(n_total, world, r) for r in range(world)]
     rows_max = max(hi - lo for lo, hi in bounds)

@@ -416,8 +416,8 @@ def test_device_result_views_and_gather(corpus_columns):
     host = pkg.propagate_batch(pkg.init_batch(corpus_columns[:, :9], precision=32),
                                np.linspace(0.0, 100.0, 7))
     assert np.array_equal(res.planes.cpu().numpy(), host.planes)
-    local, (lo, hi) = propagate_sharded(corpus_columns[:, :9], np.linspace(0.0, 100.0, 7))
-    assert (lo, hi) == shard_bounds(9, 1, 0) == (0, 9)
+    local, (axis, lo, hi) = propagate_sharded(corpus_columns[:, :9], np.linspace(0.0, 100.0, 7))
+    assert axis == "rows" and (lo, hi) == shard_bounds(9, 1, 0) == (0, 9)
     p, e = gather_grid(local.planes, local.error, 9)
     assert torch.equal(p, local.planes) and torch.equal(e, local.error)
 

@@ -13,7 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2603_27830_b200.shard import gather_grid, max_over_ranks, shard_bounds
+from paper_2603_27830_b200.shard import gather_grid, max_over_ranks, shard_bounds, shard_plan
 
 
 @pytest.mark.parametrize("n", list(range(0, 12)) + [9341, 100000])
@@ -62,5 +62,51 @@ def test_two_rank_gloo_shards_reassemble_bitwise(corpus_columns):
     mp.spawn(_worker, args=(2, _free_port(), cols, times, out), nprocs=2, join=True)
     ref_planes, ref_codes = oracle.grid(oracle.init_columns(cols, 64), times)
     assert out["slowest"] == 20.0
+    assert np.array_equal(out["planes"], ref_planes)
+    assert np.array_equal(out["codes"], ref_codes)
+
+
+@pytest.mark.parametrize("n,m,world", [(1, 1000, 8), (3, 10, 4), (9341, 1000, 8), (2, 1, 4), (0, 5, 2)])
+def test_shard_plan_covers_grid(n, m, world):
+    """Rows when there are at least as many satellites as ranks, otherwise
+    time columns (C1: one satellite on 8 GPUs); either way the shards tile
+    the grid exactly."""
+    plans = [shard_plan(n, m, world, r) for r in range(world)]
+    axes = {a for a, _, _ in plans}
+    assert len(axes) == 1
+    axis = axes.pop()
+    total = n if axis == "rows" else m
+    assert axis == ("cols" if (n < world <= m) else "rows")
+    cov = sorted((lo, hi) for _, lo, hi in plans)
+    assert cov[0][0] == 0 and cov[-1][1] == total
+    assert all(a[1] == b[0] for a, b in zip(cov, cov[1:]))
+
+
+def _col_worker(rank, world, port, cols, times, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sgp4_oracle as oracle
+        axis, lo, hi = shard_plan(cols.shape[1], times.size, world, rank)
+        assert axis == "cols"
+        planes, codes = oracle.grid(oracle.init_columns(cols, 64), times[lo:hi])
+        got = gather_grid(torch.from_numpy(planes), torch.from_numpy(codes), cols.shape[1],
+                          axis="cols", m_total=times.size)
+        if rank == 0:
+            out["planes"] = got[0].numpy()
+            out["codes"] = got[1].numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_time_shards_reassemble_bitwise(corpus_columns):
+    """One satellite on two ranks: the time axis is split and reassembled."""
+    from oracle import sgp4_oracle as oracle
+    cols = corpus_columns[:, :1]
+    times = np.linspace(0.0, 1440.0, 13)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_col_worker, args=(2, _free_port(), cols, times, out), nprocs=2, join=True)
+    ref_planes, ref_codes = oracle.grid(oracle.init_columns(cols, 64), times)
     assert np.array_equal(out["planes"], ref_planes)
     assert np.array_equal(out["codes"], ref_codes)
