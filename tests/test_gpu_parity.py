@@ -457,3 +457,55 @@ def test_fp32_kepler_classes_and_drag(oracle, corpus_columns):
     assert np.array_equal(res64.error, codes64)
     dr64, dv64 = _diff(res64.planes, ref64, ok)
     assert dr64.max() <= TOL64_R and dv64.max() <= TOL64_V
+
+
+def test_c5_full_size_properties():
+    """C5 at full size on one GPU (1,000,000 x 1,000 fp32: 28 GB of output):
+    no error codes, finite, plausible LEO radii and speeds on every cell,
+    rows sharded 8 ways into the same buffer reproduce it bitwise, and a
+    random sample of cells agrees with the oracle's fp64 path."""
+    import torch
+    from oracle import sgp4_oracle as oracle
+    from paper_2603_27830_b200 import _device
+    from paper_2603_27830_b200.catalog import starlink_like
+    from paper_2603_27830_b200.shard import shard_bounds
+    pkg = _gpu()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40e9:
+        pytest.skip("needs ~30 GB of free HBM")
+    n, m = 1_000_000, 1000
+    cols = starlink_like(n)
+    times = np.linspace(0.0, 1440.0, m)
+    sats = pkg.init_batch(cols, precision=32)
+    res = pkg.propagate_batch_device(sats, times)
+    assert int(torch.count_nonzero(res.error)) == 0
+    for p0 in (0, 3):
+        norm = torch.linalg.vector_norm(res.planes[p0:p0 + 3].float(), dim=0)
+        lo, hi = float(norm.min()), float(norm.max())
+        assert np.isfinite(lo) and np.isfinite(hi)
+        if p0 == 0:
+            assert 6650 < lo and hi < 7050
+        else:
+            assert 7.2 < lo and hi < 7.95
+        del norm
+    # 8 row shards launched into a second buffer equal the single launch
+    t_d = torch.from_numpy(times.astype(np.float32)).cuda()
+    planes2 = torch.empty_like(res.planes)
+    codes2 = torch.empty_like(res.error)
+    for r in range(8):
+        a, b = shard_bounds(n, 8, r)
+        _device.propagate_grid(sats.device_satrec, t_d, planes2[:, a:b], codes2[a:b],
+                               rows=(a, b))
+    assert torch.equal(planes2, res.planes) and torch.equal(codes2, res.error)
+    del planes2, codes2
+    rng = np.random.default_rng(11)
+    ii = rng.integers(0, n, 3000)
+    jj = rng.integers(0, m, 3000)
+    sat = oracle.init_columns(cols[:, ii], 64)
+    ref_r, ref_v, ref_c = oracle.propagate_merged(sat, times[jj])
+    got = res.planes[:, torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda()].cpu().numpy()
+    assert (ref_c == 0).all()
+    dr = np.linalg.norm(got[:3].T.astype(np.float64) - ref_r, axis=1)
+    print(f"\nC5 fp32 sample vs oracle fp64: median {np.median(dr) * 1e3:.2f} m, "
+          f"max {dr.max() * 1e3:.2f} m")
+    assert dr.max() < 0.2
