@@ -1267,6 +1267,11 @@ constexpr int kCellsPerWarp = 32 * kCellsPerLane;   // one work item (chunk)
 #define SGP4B_BLOCK 512     // one 16-warp block per SM: its warps own adjacent rows
 #endif
 constexpr int kGridBlock = SGP4B_BLOCK;
+#ifndef SGP4B_BLOCK64
+#define SGP4B_BLOCK64 SGP4B_BLOCK
+#endif
+template <typename T>
+__host__ __device__ constexpr int grid_block() { return sizeof(T) == 4 ? SGP4B_BLOCK : SGP4B_BLOCK64; }
 constexpr int kGridMinBlocks = SGP4B_MINB;   // resident blocks per SM (fp32)
 
 __device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
@@ -1526,13 +1531,14 @@ __device__ unsigned long long g_timeline[kTimelineWarps][4];
 #endif
 
 template <typename T, bool VEC, bool LO>
-__global__ void __launch_bounds__(kGridBlock, sizeof(T) == 4 ? kGridMinBlocks : kGridMinBlocks64)
+__global__ void __launch_bounds__(grid_block<T>(), sizeof(T) == 4 ? kGridMinBlocks : kGridMinBlocks64)
 grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t n,
             const T* __restrict__ times, const float* __restrict__ times_lo, int64_t times_ld,
             int64_t m, Grav g, T* __restrict__ planes, int64_t plane_stride, int64_t row_stride,
             int32_t* __restrict__ codes, int64_t code_stride, int64_t chunks) {
-  const int64_t nwarps = (int64_t)gridDim.x * (kGridBlock / 32);
-  const int64_t w = ((int64_t)blockIdx.x * kGridBlock + threadIdx.x) >> 5;
+  constexpr int kBlock = grid_block<T>();
+  const int64_t nwarps = (int64_t)gridDim.x * (kBlock / 32);
+  const int64_t w = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t total = n * chunks;
   const int64_t g0 = total * w / nwarps;
@@ -1540,7 +1546,7 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
 
   constexpr bool kSmem = sizeof(T) == 8 ? SGP4B_SMEM_REC64 : SGP4B_SMEM_REC;
   constexpr bool kShfl = sizeof(T) == 4 && SGP4B_SHFL_REC;
-  __shared__ __align__(16) T srec[kSmem ? kGridBlock / 32 : 1][S_COUNT];
+  __shared__ __align__(16) T srec[kSmem ? kBlock / 32 : 1][S_COUNT];
   T* my = srec[kSmem ? (threadIdx.x >> 5) : 0];
   using RecT = typename std::conditional<
       kShfl, RecW, typename std::conditional<kSmem, RecS<T>, Rec<T>>::type>::type;
@@ -1666,7 +1672,8 @@ int64_t resident_blocks(int precision) {
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const void* fn = precision == 64 ? (const void*)grid_kernel<double, true, false>
                                     : (const void*)grid_kernel<float, true, false>;
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridBlock, 0);
+  const int block = precision == 64 ? grid_block<double>() : grid_block<float>();
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, 0);
   if (e != cudaSuccess || sms <= 0 || per_sm <= 0) {
     fail(SGP4B_ECUDA, "occupancy query: %s", cudaGetErrorString(e));
     return -1;
@@ -1682,13 +1689,14 @@ int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* 
                 int64_t code_stride, bool vec, cudaStream_t s, const char* what) {
   const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
   const int64_t warps = n * chunks;
-  int64_t blocks = (warps * 32 + kGridBlock - 1) / kGridBlock;
+  const int block = precision == 64 ? grid_block<double>() : grid_block<float>();
+  int64_t blocks = (warps * 32 + block - 1) / block;
   const int64_t slots = resident_blocks(precision);
   if (slots <= 0) return fail(SGP4B_ECUDA, "%s: %s", what, g_last_error);
   if (blocks > slots) blocks = slots;
   if (precision == 64) {
     auto k = vec ? grid_kernel<double, true, false> : grid_kernel<double, false, false>;
-    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(
+    k<<<(unsigned)blocks, block, 0, s>>>(
         static_cast<const double*>(rec), rec_idx, n, static_cast<const double*>(times), nullptr,
         times_ld, m, g, static_cast<double*>(planes), plane_stride, row_stride, codes,
         code_stride, chunks);
@@ -1696,7 +1704,7 @@ int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* 
     auto k = times_lo != nullptr
                  ? (vec ? grid_kernel<float, true, true> : grid_kernel<float, false, true>)
                  : (vec ? grid_kernel<float, true, false> : grid_kernel<float, false, false>);
-    k<<<(unsigned)blocks, kGridBlock, 0, s>>>(
+    k<<<(unsigned)blocks, block, 0, s>>>(
         static_cast<const float*>(rec), rec_idx, n, static_cast<const float*>(times), times_lo,
         times_ld, m, g, static_cast<float*>(planes), plane_stride, row_stride, codes, code_stride,
         chunks);
