@@ -65,3 +65,27 @@ def test_invalid_arguments_rejected(call):
     lib = _native.load()
     assert call(lib) == -1
     assert lib.sgp4b_last_error()  # message recorded
+
+
+def _sass(function_pattern: str) -> str:
+    """SASS of the library's functions whose mangled name matches."""
+    import shutil
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", str(_native.library_path())], capture_output=True,
+                         text=True, check=True).stdout
+    blocks = re.split(r"\n\s*Function : ", out)
+    return "\n".join(b for b in blocks if re.match(function_pattern, b))
+
+
+def test_fp32_grid_kernel_sass_is_the_designed_one():
+    """The shipped fp32 grid kernel is compiled for sm_100a with packed
+    dual-fp32 arithmetic (FFMA2/FMUL2), SFU transcendentals (MUFU),
+    evict-first 128-bit streaming stores, and no local-memory spills
+    (DESIGN.md §3-4): a regression guard that needs no GPU."""
+    sass = _sass(r"\S*grid_kernelIfLb1ELb0E")
+    assert sass, "grid_kernel<float, true, false> not found"
+    for op in ("FFMA2", "FMUL2", "MUFU.SIN", "MUFU.RSQ", "STG.E.EF.128"):
+        assert op in sass, op
+    assert "STL" not in sass and "LDL" not in sass
+    # one satellite record load per row: 10 x 128-bit broadcast loads
+    assert len(re.findall(r"LDG\.E\.128\.CONSTANT", sass)) >= 10
