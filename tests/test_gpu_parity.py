@@ -509,3 +509,14 @@ def test_c5_full_size_properties():
     print(f"\nC5 fp32 sample vs oracle fp64: median {np.median(dr) * 1e3:.2f} m, "
           f"max {dr.max() * 1e3:.2f} m")
     assert dr.max() < 0.2
+
+
+def test_scaling_sweep_gpu(real_elements):
+    """The reference's sweep harness over the GPU path (bench.py:91-124)."""
+    pkg = _gpu()
+    els = list(real_elements.values())
+    recs = pkg.scaling_sweep("satellites", [3, 17], 50, els, precision=32, full_pipeline=False)
+    assert [r.n for r in recs] == [3, 17] and all(r.m == 50 for r in recs)
+    assert all(r.throughput_cells_per_s > 0 and r.trials == 5 for r in recs)
+    from paper_2603_27830_b200.timing import emit_bench_csv
+    assert emit_bench_csv(recs).splitlines()[1].startswith("satellites-3,satellites,3,50,32")

@@ -150,3 +150,46 @@ def test_bench_reference_arm_nonzero_rank_is_silent():
                           "--steps", "1", "--warmup", "0", "--ref-rows", "8"],
                          capture_output=True, text=True, timeout=300, cwd=root, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_time_task_protocol_and_failures():
+    """The reference timing protocol (bench.py:48-82): warm-up, doubling
+    until the fastest of five trials clears 0.2 s, min per iteration."""
+    import time as _t
+    from paper_2603_27830_b200 import BenchRecord, TaskFailed, time_task
+    calls = []
+
+    def task():
+        calls.append(1)
+        _t.sleep(0.03)
+    rec = time_task(task, label="sleep", n=3, m=4, precision=32)
+    assert isinstance(rec, BenchRecord) and rec.trials == 5 and rec.total_cells == 12
+    assert rec.iterations & (rec.iterations - 1) == 0            # a power of two
+    assert rec.iterations * rec.min_time_s > 0.2
+    assert 0.03 <= rec.min_time_s < 0.06
+    assert rec.throughput_cells_per_s == 12 / rec.min_time_s
+
+    state = {"k": 0}
+
+    def flaky():
+        state["k"] += 1
+        if state["k"] == 3:
+            raise KeyError("boom")
+    with pytest.raises(TaskFailed) as ei:
+        time_task(flaky)
+    assert ei.value.trial_index == 0 and isinstance(ei.value.__cause__, KeyError)
+
+    def broken():
+        raise ValueError("warm-up")
+    with pytest.raises(ValueError):                               # warm-up is not wrapped
+        time_task(broken)
+
+
+def test_scaling_sweep_validation():
+    from paper_2603_27830_b200 import scaling_sweep
+    with pytest.raises(ValueError):
+        scaling_sweep("cells", [1, 2], 10, [])
+    with pytest.raises(ValueError):
+        scaling_sweep("times", [4, 2], 10, [])
+    with pytest.raises(ValueError):
+        scaling_sweep("times", [2, 2], 10, [])
