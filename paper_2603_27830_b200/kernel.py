@@ -231,10 +231,10 @@ def _grid_of_rows(dev, rows: np.ndarray, times: np.ndarray):
     ``propagate_batch`` (so results equal the batch bit for bit)."""
     from .batch import _alloc_grid
     device = dev.device
-    rows_d = torch.from_numpy(rows).to(device)
+    rows_d = torch.from_numpy(np.array(rows, dtype=np.int64)).to(device)
     sub = dataclasses.replace(dev, record=dev.record.index_select(0, rows_d).contiguous(),
                               codes=dev.codes.index_select(0, rows_d))
-    t_d = torch.from_numpy(times).to(device)
+    t_d = torch.from_numpy(np.array(times)).to(device)
     planes, codes = _alloc_grid(int(rows.size), int(times.size), dev.precision, device)
     _device.propagate_grid(sub, t_d, planes, codes)
     return planes, codes
