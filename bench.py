@@ -278,10 +278,17 @@ def run_ours(args, world, rank, local) -> None:
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    # one process per GPU; SGP4B_BENCH_BACKEND=gloo (test only) lets several
+    # ranks share a GPU to exercise the multi-rank plumbing on a 1-GPU box
+    backend = os.environ.get("SGP4B_BENCH_BACKEND", "nccl")
+    gpu = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(gpu)
+    device = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     desc, nsat, tfn, default_prec = WORKLOADS[args.workload]
     precision = args.precision or default_prec
@@ -318,7 +325,7 @@ def run_ours(args, world, rank, local) -> None:
     def launch():
         _device.propagate_grid(sats.device_satrec, t_dev, planes, error)
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     sampler.__enter__()
     for _ in range(max(args.warmup, 3)):
         flush_l2(0)
