@@ -128,9 +128,10 @@ def pack_device(satrec64: np.ndarray, codes: np.ndarray, isimp: np.ndarray,
     """Host SoA fields (e.g. from a user-built SatInit) -> packed records."""
     device = require_cuda(device)
     n = satrec64.shape[1]
-    sr = torch.from_numpy(np.ascontiguousarray(satrec64, dtype=np.float64)).to(device)
-    cd = torch.from_numpy(np.ascontiguousarray(codes, dtype=np.int32)).to(device)
-    si = torch.from_numpy(np.ascontiguousarray(isimp, dtype=np.uint8)).to(device)
+    # np.array copies: the SatInit fields may be read-only views
+    sr = torch.from_numpy(np.array(satrec64, dtype=np.float64, order="C")).to(device)
+    cd = torch.from_numpy(np.array(codes, dtype=np.int32, order="C")).to(device)
+    si = torch.from_numpy(np.array(isimp, dtype=np.uint8, order="C")).to(device)
     record = torch.empty((n, RECORD_SLOTS), dtype=torch_dtype(precision), device=device)
     g = _grav_host(grav, device)
     with torch.cuda.device(device):

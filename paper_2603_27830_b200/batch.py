@@ -151,7 +151,7 @@ def init_batch(elements: Sequence[MeanElements], grav: GravityModel = WGS72,
 
 
 def _times(sats: SatBatch, times) -> np.ndarray:
-    t = np.asarray(times, dtype=sats.dtype)
+    t = np.array(times, dtype=sats.dtype)          # own, writable copy (M values)
     if t.ndim != 1 or t.size == 0:
         raise ValueError("times must be a non-empty 1-D array")
     return t
@@ -268,7 +268,7 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
     """
     if tile_rows < 1 or tile_cols < 1:
         raise ValueError("tile dimensions must be >= 1")
-    t = np.asarray(times, dtype=sats.dtype)
+    t = np.array(times, dtype=sats.dtype)
     if t.ndim != 1:
         raise ValueError("times must be a 1-D array")
     dev = sats.device_satrec

@@ -213,7 +213,7 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
         idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape),
                               out_shape).ravel()
         tt = np.ascontiguousarray(np.broadcast_to(t, out_shape).ravel())
-        idx_d = torch.from_numpy(np.ascontiguousarray(idx)).to(device)
+        idx_d = torch.from_numpy(np.array(idx)).to(device)
         t_d = torch.from_numpy(tt).to(device)
         rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
         codes = torch.empty((p,), dtype=torch.int32, device=device)
@@ -249,7 +249,7 @@ def solve_kepler(axnl, aynl, u_init):
         dtype = np.float64
     precision = _device.precision_of(dtype)
     device = _device.require_cuda()
-    tens = [torch.from_numpy(np.ascontiguousarray(x, dtype=dtype).ravel()).to(device)
+    tens = [torch.from_numpy(np.array(x, dtype=dtype).ravel()).to(device)
             for x in (a, b, u)]
     if tens[0].numel() == 0:
         return np.empty(a.shape, dtype=dtype)
