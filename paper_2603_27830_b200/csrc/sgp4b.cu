@@ -1399,6 +1399,8 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
   T th[kCellsPerLane];
   float tl[kCellsPerLane];
   load_times(j0, th, tl);
+  T* pb = row + j0;                          // output pointers walk the row
+  int32_t* cb = crow + j0;
   for (int64_t c = c0; c < c1; ++c, j0 += kCellsPerWarp) {
 #if SGP4B_SHFL_REC
     // keep the warp converged (record fields are shuffled): lanes past the
@@ -1438,8 +1440,10 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     }
 #endif
 
-    T* base = row + j0;
-    int32_t* cbase = crow + j0;
+    T* base = pb;
+    int32_t* cbase = cb;
+    pb += kCellsPerWarp;
+    cb += kCellsPerWarp;
     if (full) {
 #pragma unroll
       for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
