@@ -42,6 +42,8 @@ PAPER_A100_PROPS = 9341 * 1000 / 3.8e-3          # PAPER.md:99, 3.8 ms on A100
 
 WORKLOADS = {
     # name: (description, sats per rank, times, default precision)
+    "c1": ("C1 ISS 1 sat x 1,000 steps (linspace 0..1440 min) fp64", 1,
+           lambda: np.linspace(0.0, 1440.0, 1000), 64),
     "c2": ("C2 Starlink-like 9,341 sats x 1,000 steps (linspace 0..1440 min)", 9341,
            lambda: np.linspace(0.0, 1440.0, 1000), 32),
     "c3": ("C3 Starlink-like 9,341 sats x 1,000 steps fp64", 9341,
@@ -239,8 +241,12 @@ def run_reference(args, world, rank) -> None:
     # bounded sample: ~2e9 cells over the whole --steps/--warmup run (about a
     # minute on 16 host threads), at most the workload's own catalogue
     budget_rows = int(2.0e9 / max(1, args.steps + args.warmup) / times.size)
-    rows = max(16, min(nsat, args.ref_rows, budget_rows))
-    cols = starlink_like(rows)
+    rows = max(1, min(nsat, args.ref_rows, budget_rows))
+    if args.workload == "c1":
+        from paper_2603_27830_b200.catalog import iss_columns
+        cols = iss_columns()
+    else:
+        cols = starlink_like(rows)
     workers = oracle.default_workers()
 
     def step():
@@ -294,7 +300,15 @@ def run_ours(args, world, rank, local) -> None:
     precision = args.precision or default_prec
     times = tfn()
     m = times.size
-    if args.workload in ("c4", "c5"):        # fixed total, sharded (strong scaling)
+    if args.workload == "c1":                # one satellite: ranks split the time axis
+        from paper_2603_27830_b200.catalog import iss_columns
+        from paper_2603_27830_b200.shard import shard_plan
+        cols = iss_columns()
+        _, lo, hi = shard_plan(1, times.size, world, rank)
+        times = times[lo:hi] if world > 1 else times
+        m = times.size
+        scaling = "strong"
+    elif args.workload in ("c4", "c5"):      # fixed total, sharded (strong scaling)
         lo = nsat * rank // world
         hi = nsat * (rank + 1) // world
         cols = starlink_like(nsat)[:, lo:hi]

@@ -80,3 +80,15 @@ def starlink_like(n: int, seed: int = SEED, base: int = 9341) -> np.ndarray:
         return cols
     reps = -(-n // k)
     return np.tile(cols, (1, reps))[:, :n].copy()
+
+
+# C1 (BASELINE.json configs[0]): the reference's ISS fixture record
+# (tests/conftest.py:77-79 of the reference; tests/golden/real_tles.tle here)
+ISS_LINES = ("1 25544U 98067A   20344.91667824  .00016717  00000-0  10270-3 0  9003",
+             "2 25544  51.6442  21.0000 0001882 345.0000  15.0000 15.49309239  1000")
+
+
+def iss_columns() -> np.ndarray:
+    """(7, 1) fp64 element columns of the C1 ISS record."""
+    from .tle import parse_catalog_columns
+    return parse_catalog_columns([ISS_LINES[0]], [ISS_LINES[1]])
