@@ -520,3 +520,30 @@ def test_scaling_sweep_gpu(real_elements):
     assert all(r.throughput_cells_per_s > 0 and r.trials == 5 for r in recs)
     from paper_2603_27830_b200.timing import emit_bench_csv
     assert emit_bench_csv(recs).splitlines()[1].startswith("satellites-3,satellites,3,50,32")
+
+
+def test_streamed_memory_contract(corpus_columns):
+    """propagate_batch_streamed keeps O(tile) host memory (the reference's
+    tracemalloc contract, test_batch.py:152-173): the pinned host peak while
+    streaming a 2,000 x 2,000 grid (112 MB dense) in 100 x 500 tiles stays
+    within a few tiles, and no dense device grid is allocated either."""
+    import torch
+    pkg = _gpu()
+    sats = pkg.init_batch(np.tile(corpus_columns, (1, 2))[:, :2000], precision=32)
+    times = np.linspace(0.0, 1440.0, 2000)
+    tile_bytes = 100 * 500 * 28
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_host_memory_stats()
+    torch.cuda.reset_peak_memory_stats()
+    host0 = torch.cuda.host_memory_stats().get("allocated_bytes.all.current", 0)
+    dev0 = torch.cuda.memory_allocated()
+    count = [0]
+
+    def sink(rows, cols, planes, error):
+        count[0] += 1
+    summary = pkg.propagate_batch_streamed(sats, times, 100, 500, sink)
+    assert count[0] == 20 * 4 and summary.cells_emitted == 2000 * 2000
+    host_peak = torch.cuda.host_memory_stats().get("allocated_bytes.all.peak", 0) - host0
+    dev_peak = torch.cuda.max_memory_allocated() - dev0
+    assert host_peak <= 4 * tile_bytes, host_peak
+    assert dev_peak <= 8 * tile_bytes + (1 << 20), dev_peak
