@@ -70,7 +70,7 @@ def test_fp64_matches_reference_goldens(golden_columns, golden_states):
 def test_fp32_codes_and_accuracy(oracle, corpus_columns, corpus_ref64):
     pkg = _gpu()
     times, (ref64, codes64) = corpus_ref64
-    _, codes32 = oracle.grid(oracle.init_columns(corpus_columns, 32), times, workers=4)
+    ref32, codes32 = oracle.grid(oracle.init_columns(corpus_columns, 32), times, workers=4)
     res = pkg.propagate_batch(pkg.init_batch(corpus_columns, precision=32), times)
     assert res.planes.dtype == np.float32
     assert np.array_equal(res.error, codes64)
@@ -81,6 +81,10 @@ def test_fp32_codes_and_accuracy(oracle, corpus_columns, corpus_ref64):
           f"{np.median(dr) * 1e3:.2f} m p99 {np.percentile(dr, 99) * 1e3:.2f} m max "
           f"{dr.max() * 1e3:.2f} m; |dv| max {dv.max() * 1e3:.4f} m/s")
     assert np.median(dr) < 0.05 and dr.max() < 1.0 and dv.max() < 1e-3
+    # and well inside the reference's own fp32 error on the same cells
+    dr_ref, _ = _diff(ref32, ref64, ok)
+    assert np.median(dr) < 0.5 * np.median(dr_ref)
+    assert np.percentile(dr, 99) < 0.5 * np.percentile(dr_ref, 99) and dr.max() < dr_ref.max()
 
 
 def test_fp32_goldens_codes(golden_columns, golden_states):
