@@ -752,7 +752,7 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 rsam2 = rsam * rsam;                                   // 1 / am
   V2 ilp;                                                         // 1 / pl_lp
   if constexpr (KITER == 1) {
-    // e < 0.004 (+ drag margin): 1 / (am (1 - em^2)) = (1 + em^2) / am
+    // class 1 (e < 0.003): 1 / (am (1 - em^2)) = (1 + em^2) / am
     // to O(em^4) < 1e-9, the guard pl_lp > tiny is implied
     ilp = fma2(em, em, 1.0f) * rsam2;
   } else {
