@@ -793,11 +793,11 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     else eo1 = eo1 + tem5;
   }
   V2 sineo1, coseo1;
-  if constexpr (KITER == 1) {
-    // E = u + tem5 straight through the SFU: the FMA pipe is the binding
+  if constexpr (KITER == 1 || KITER == 2) {
+    // E = u + d straight through the SFU: the FMA pipe is the binding
     // resource and the XU has room (12 vs 10 MUFU per cell measured 2 %
     // faster than the 6-op rotation); accuracy is the same SFU-level
-    sincos2(u + tem5, sineo1, coseo1);
+    sincos2(u + d, sineo1, coseo1);
   } else if constexpr (KITER > 0) {
     rotate_tiny(s, c, tem5, sineo1, coseo1);     // last step <= e^3/2 < 4e-3
   } else {
