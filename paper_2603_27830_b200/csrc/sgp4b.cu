@@ -49,6 +49,9 @@
 #ifndef SGP4B_SHFL_REC
 #define SGP4B_SHFL_REC 0          // fp32 records spread over the warp (shfl at use)
 #endif
+#ifndef SGP4B_K2_SERIES
+#define SGP4B_K2_SERIES 1           // class-2 (e < 0.1) series for 1/pl_lp, 1/den, 1/(1+betal)
+#endif
 #ifndef SGP4B_SMEM_REC64
 #define SGP4B_SMEM_REC64 1        // fp64 records (80 registers) in shared memory
 #endif
@@ -755,6 +758,11 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     // class 1 (e < 0.003): 1 / (am (1 - em^2)) = (1 + em^2) / am
     // to O(em^4) < 1e-9, the guard pl_lp > tiny is implied
     ilp = fma2(em, em, 1.0f) * rsam2;
+  } else if constexpr (KITER == 2 && SGP4B_K2_SERIES) {
+    // class 2 (e < 0.1): (1 + em^2 + em^4) / am, truncation em^6 < 1e-6
+    // relative on terms of order 1e-3 (aycof, xlcof)
+    const V2 em2 = em * em;
+    ilp = fma2(em2, em2 + 1.0f, 1.0f) * rsam2;
   } else {
     ilp = rcp2(vmax(am * fma2(-em, em, 1.0f), tiny));
   }
@@ -782,6 +790,13 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
       // den = 1 - q with |q| <= e < 0.004: 1/den = 1 + q + q^2 to O(q^3)
       const V2 q = fma2(c, axnl, s * aynl);
       tem5 = num * fma2(q, q + 1.0f, 1.0f);
+    } else if constexpr (KITER == 2 && SGP4B_K2_SERIES) {
+      // |q| <= e < 0.1: the first step's 1 + q + q^2 (error q^3 e) is
+      // absorbed by the second Newton step, the last step's 1 + q + q^2 + q^3
+      // leaves q^4 of a step below e^3/2
+      const V2 q = fma2(c, axnl, s * aynl);
+      const V2 q1 = q + 1.0f;
+      tem5 = num * (it == 0 ? fma2(q, q1, 1.0f) : fma2(q, fma2(q, q1, 1.0f), 1.0f));
     } else {
       const V2 den = fma2(-s, aynl, fma2(-c, axnl, 1.0f));
       tem5 = num * rcp2(den);
@@ -830,7 +845,12 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
     for (int k = 0; k < NC; ++k) bad_pl[k] = comp(omel2, k) < 0.0f;
     const V2 rb = rsq2(omel2);
     betal = omel2 * rb;
-    tq = esine * rcp2(betal + 1.0f);
+    if constexpr (SGP4B_K2_SERIES) {
+      // 1/(1 + sqrt(1-x)) = 1/2 + x/8 + x^2/16 + O(5x^3/128), x = el2 < 0.0121
+      tq = esine * fma2(el2, fma2(el2, 0.0625f, 0.125f), 0.5f);
+    } else {
+      tq = esine * rcp2(betal + 1.0f);
+    }
     const V2 rspl = rsam * rb;
     ipl = rspl * rspl;
   } else {
