@@ -1508,9 +1508,9 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
                                              int lane, const float* times, const float* times_lo,
                                              int64_t m, float* row, int64_t ps, int32_t* crow) {
 #ifdef SGP4B_ONLY_CLASS_K1
-  // analysis build: every row runs the (non-isimp, Kepler 1) instance, so the
-  // SASS holds one chunk loop (static instruction mix per cell)
-  row32<false, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  // analysis build: every row runs the (non-isimp, Kepler SGP4B_ONLY_CLASS_K1)
+  // instance, so the SASS holds one chunk loop (static instruction mix)
+  row32<false, SGP4B_ONLY_CLASS_K1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
   return;
 #endif
   const int flags = R.flags();
