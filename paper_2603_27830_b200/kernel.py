@@ -212,7 +212,7 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
         # general broadcast: one (satellite, time) pair per cell
         idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape),
                               out_shape).ravel()
-        tt = np.ascontiguousarray(np.broadcast_to(t, out_shape).ravel())
+        tt = np.array(np.broadcast_to(t, out_shape).ravel())          # writable copy
         idx_d = torch.from_numpy(np.array(idx)).to(device)
         t_d = torch.from_numpy(tt).to(device)
         rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
