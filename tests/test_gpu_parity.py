@@ -551,3 +551,29 @@ def test_streamed_memory_contract(corpus_columns):
     dev_peak = torch.cuda.max_memory_allocated() - dev0
     assert host_peak <= 4 * tile_bytes, host_peak
     assert dev_peak <= 8 * tile_bytes + (1 << 20), dev_peak
+
+
+def test_bench_json_contract():
+    """bench.py prints one JSON line with the driver's keys (N=1)."""
+    import json
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "5", "--warmup", "3",
+                          "--e2e-steps", "1", "--no-cpu"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["gpu_launches"] == 5
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 9341 * 1000 * 28
+    assert "workload" in d["config"] and d["value"] > 1e10
