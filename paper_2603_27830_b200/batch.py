@@ -308,19 +308,26 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
             planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
             _device.propagate_grid(dev, t_d[cols].clone(), planes_d, err_d,
                                    rows=(rows.start, rows.stop))
-            planes_h, err_h = _alloc_grid(tr, tc, dev.precision, "cpu", pin=True)
+            # as in propagate_batch, code rows cross PCIe only where nonzero
+            flags_h = torch.empty((tr,), dtype=torch.bool, pin_memory=True)
+            flags_h.copy_(err_d.ne(0).any(dim=1), non_blocking=True)
+            planes_h = _alloc_host_planes(tr, tc, dev.precision)
             planes_h.copy_(planes_d, non_blocking=True)
-            err_h.copy_(err_d, non_blocking=True)
             done = torch.cuda.Event()
             done.record(stream)
-            return planes_h, err_h, done, (planes_d, err_d)
+            return planes_h, flags_h, done, (planes_d, err_d)
 
         pending = launch(tiles[0])
         for k, (rows, cols) in enumerate(tiles):
-            planes_h, err_h, done, _keep = pending
+            planes_h, flags_h, done, keep = pending
             pending = launch(tiles[k + 1]) if k + 1 < len(tiles) else None
             done.synchronize()
-            planes_np, err_np = planes_h.numpy(), err_h.numpy()
+            planes_np = planes_h.numpy()
+            err_np = np.zeros((rows.stop - rows.start, cols.stop - cols.start), dtype=np.int32)
+            bad = np.flatnonzero(flags_h.numpy())
+            if bad.size:
+                idx = torch.from_numpy(bad.astype(np.int64)).to(dev.device)
+                err_np[bad] = keep[1].index_select(0, idx).cpu().numpy()
             try:
                 sink(rows, cols, planes_np, err_np)
             except Exception as exc:

@@ -577,3 +577,28 @@ def test_bench_json_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 9341 * 1000 * 24 + 9341
     assert "workload" in d["config"] and d["value"] > 1e10
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_sparse_code_rows_with_errors(failure_table, corpus_columns, precision):
+    """propagate_batch / propagate_batch_streamed move only the code rows that
+    hold a nonzero code; with failure-mode satellites mixed into a corpus
+    the host code planes still equal the device grid exactly."""
+    import torch
+    pkg = _gpu()
+    bad = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    cols = np.concatenate([corpus_columns[:, :5], bad, corpus_columns[:, 5:9]], axis=1)
+    times = np.array(failure_table["times"] + [4000.0, 9000.0])
+    sats = pkg.init_batch(cols, precision=precision)
+    host = pkg.propagate_batch(sats, times)
+    dev = pkg.propagate_batch_device(sats, times)
+    assert np.count_nonzero(host.error) > 0
+    assert np.array_equal(host.error, dev.error.cpu().numpy())
+    assert np.array_equal(host.planes, dev.planes.cpu().numpy(), equal_nan=True)
+    got = np.full_like(host.error, -1)
+
+    def sink(rows, cols_, planes, error):
+        got[rows, cols_] = error
+    summary = pkg.propagate_batch_streamed(sats, times, 3, 4, sink)
+    assert np.array_equal(got, host.error)
+    assert summary.nonzero_error_count == int(np.count_nonzero(host.error))
