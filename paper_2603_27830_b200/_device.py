@@ -100,7 +100,9 @@ def init_device(elements: np.ndarray, grav: GravityModel, precision: int,
                 device=None) -> DeviceSatrec:
     """(7, n) fp64 element columns -> DeviceSatrec via the init kernel."""
     device = require_cuda(device)
-    elements = np.array(elements, dtype=np.float64, order="C")   # own writable copy
+    elements = np.ascontiguousarray(elements, dtype=np.float64)
+    if not elements.flags.writeable:                  # torch.from_numpy wants writable
+        elements = elements.copy()
     n = elements.shape[1]
     el = torch.from_numpy(elements).to(device, non_blocking=False)
     return init_device_tensor(el, grav, precision, device)
