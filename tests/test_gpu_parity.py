@@ -602,3 +602,27 @@ def test_sparse_code_rows_with_errors(failure_table, corpus_columns, precision):
     summary = pkg.propagate_batch_streamed(sats, times, 3, 4, sink)
     assert np.array_equal(got, host.error)
     assert summary.nonzero_error_count == int(np.count_nonzero(host.error))
+
+
+@pytest.mark.parametrize("n,m", [(1, 1_000_000), (200_000, 1), (3, 130)])
+def test_extreme_grid_shapes(oracle, corpus_columns, n, m):
+    """One satellite over a million steps (work split along the time axis
+    inside one row), 200,000 one-step rows, and a row that ends two cells
+    into its second chunk: sampled cells equal the oracle's codes and stay
+    within the fp32 bound."""
+    import torch
+    pkg = _gpu()
+    cols = np.tile(corpus_columns, (1, -(-n // corpus_columns.shape[1])))[:, :n]
+    times = np.linspace(-720.0, 2880.0, m)
+    res = pkg.propagate_batch_device(pkg.init_batch(cols, precision=32), times)
+    rng = np.random.default_rng(n + m)
+    ii = rng.integers(0, n, 500)
+    jj = rng.integers(0, m, 500)
+    sat = oracle.init_columns(cols[:, ii], 64)
+    ref_r, _, ref_c = oracle.propagate_merged(sat, times[jj])
+    got = res.planes[:, torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda()].cpu().numpy()
+    codes = res.error[torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda()].cpu().numpy()
+    assert np.array_equal(codes, ref_c)
+    ok = ref_c == 0
+    dr = np.linalg.norm(got[:3].T[ok].astype(np.float64) - ref_r[ok], axis=1)
+    assert dr.max() < 0.5
