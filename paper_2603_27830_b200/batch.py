@@ -230,7 +230,8 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchR
         t_d = t_h.to(dev.device, non_blocking=True)
         res = propagate_batch_device(sats, t_d)
         flags_h = torch.empty((n,), dtype=torch.bool, pin_memory=True)
-        flags_h.copy_(res.error.ne(0).any(dim=1), non_blocking=True)
+        # codes are >= 0, so a row max is the flag (no grid-sized temporary)
+        flags_h.copy_(res.error.amax(dim=1) > 0, non_blocking=True)
         planes_h = _alloc_host_planes(n, m, dev.precision)
         planes_h.copy_(res.planes, non_blocking=True)
         stream.synchronize()
@@ -310,7 +311,7 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
                                    rows=(rows.start, rows.stop))
             # as in propagate_batch, code rows cross PCIe only where nonzero
             flags_h = torch.empty((tr,), dtype=torch.bool, pin_memory=True)
-            flags_h.copy_(err_d.ne(0).any(dim=1), non_blocking=True)
+            flags_h.copy_(err_d.amax(dim=1) > 0, non_blocking=True)
             planes_h = _alloc_host_planes(tr, tc, dev.precision)
             planes_h.copy_(planes_d, non_blocking=True)
             done = torch.cuda.Event()
