@@ -195,6 +195,14 @@ def time_task_cpu(task, min_trial_s: float = 0.2, trials: int = 5) -> float:
 
 
 def cpu_model() -> str:
+    """lscpu's model name (BASELINE.md §3), else /proc/cpuinfo's."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.strip().startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
     try:
         for ln in open("/proc/cpuinfo"):
             if ln.startswith("model name"):
@@ -204,21 +212,63 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(cols: np.ndarray, times: np.ndarray, precision: int, max_rows: int) -> dict:
+def cpu_baseline(cols: np.ndarray, times: np.ndarray, precision: int, max_rows: int,
+                 rows_1thread: int = 1000) -> dict:
     """The reference CPU path (oracle/ port, bit-exact with sgp4kit) on a
-    bounded sample of the same workload, all host threads."""
+    bounded sample of the same workload, timed with the reference's own
+    time_task protocol: all host threads, and one thread."""
     from oracle import sgp4_oracle as oracle
     workers = oracle.default_workers()
     rows = min(cols.shape[1], max_rows)
-    sub = cols[:, :rows]
-    sat = oracle.init_columns(sub, precision)
+    sat = oracle.init_columns(cols[:, :rows], precision)
     per = time_task_cpu(lambda: oracle.grid(sat, times, workers=workers))
+    r1 = min(cols.shape[1], rows_1thread)
+    sat1 = oracle.init_columns(cols[:, :r1], precision)
+    per1 = time_task_cpu(lambda: oracle.grid(sat1, times, workers=1))
     cells = rows * times.size
+    model = cpu_model()
     return {"value": cells / per, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": f"{rows} sats x {times.size} steps fp{precision}, propagate-only, "
-                      f"reference time_task protocol (min of 5), numpy {np.__version__}, "
-                      f"{cpu_model()}",
-            "ms_per_run": per * 1e3}
+                      f"reference time_task protocol (min of 5), {workers} threads; "
+                      f"numpy {np.__version__}, {model}",
+            "ms_per_run": per * 1e3,
+            "value_1thread": r1 * times.size / per1,
+            "sample_1thread": f"{r1} sats x {times.size} steps fp{precision}, 1 thread",
+            "cpu_model": model, "os_cpu_count": os.cpu_count(), "numpy": np.__version__}
+
+
+def bench_config(workload: str, desc: str, n: int, m: int, precision: int, world: int,
+                 scaling: str) -> dict:
+    """The workload description both arms print (identical dicts, so the
+    driver can match the two lines)."""
+    return {"workload": desc, "workload_id": workload, "n_sats_per_gpu": n, "n_steps": m,
+            "cells_per_gpu": n * m, "precision": f"fp{precision}",
+            "parallelism": f"satellite shards x{world}, no collective",
+            "scaling": scaling, "catalogue": "synthetic Starlink-like (catalog.starlink_like, "
+                                             "seed 20260113)" if workload != "c1" else "ISS",
+            "l2": "GPU arm: L2 flushed before every timed launch (256 MiB write, then 256 MiB "
+                  "read); outputs exceed L2 for C2-C5"}
+
+
+def workload_shape(workload: str, world: int, rank: int):
+    """(description, element columns of this rank, times, precision default,
+    scaling) for a workload, identical in both arms."""
+    from paper_2603_27830_b200.catalog import SEED, starlink_like
+    desc, nsat, tfn, default_prec = WORKLOADS[workload]
+    times = tfn()
+    if workload == "c1":                # one satellite: ranks split the time axis
+        from paper_2603_27830_b200.catalog import iss_columns
+        from paper_2603_27830_b200.shard import shard_plan
+        cols = iss_columns()
+        _, lo, hi = shard_plan(1, times.size, world, rank)
+        times = times[lo:hi] if world > 1 else times
+        return desc, cols, times, default_prec, "strong"
+    if workload in ("c4", "c5"):        # fixed total, sharded (strong scaling)
+        lo = nsat * rank // world
+        hi = nsat * (rank + 1) // world
+        return desc, starlink_like(nsat)[:, lo:hi], times, default_prec, "strong"
+    # per-rank Starlink shard (weak scaling)
+    return desc, starlink_like(nsat, seed=SEED + rank), times, default_prec, "weak"
 
 
 def dist_setup():
@@ -230,27 +280,23 @@ def dist_setup():
 
 def run_reference(args, world, rank) -> None:
     """--impl reference: the reference CPU implementation of the path (the
-    oracle port, bit-exact with sgp4kit) on the host cores, rank 0 only."""
+    oracle port, bit-exact with sgp4kit) on the host cores, rank 0 only, on
+    this arm's workload (bounded sample per step)."""
     if rank != 0:
         return
     from oracle import sgp4_oracle as oracle
-    from paper_2603_27830_b200.catalog import starlink_like
-    desc, nsat, tfn, default_prec = WORKLOADS[args.workload]
+    desc, cols, times, default_prec, scaling = workload_shape(args.workload, world, 0)
     precision = args.precision or default_prec
-    times = tfn()
+    nsat = cols.shape[1]
     # bounded sample: ~2e9 cells over the whole --steps/--warmup run (about a
     # minute on 16 host threads), at most the workload's own catalogue
     budget_rows = int(2.0e9 / max(1, args.steps + args.warmup) / times.size)
     rows = max(1, min(nsat, args.ref_rows, budget_rows))
-    if args.workload == "c1":
-        from paper_2603_27830_b200.catalog import iss_columns
-        cols = iss_columns()
-    else:
-        cols = starlink_like(rows)
+    sub = cols[:, :rows]
     workers = oracle.default_workers()
 
     def step():
-        sat = oracle.init_columns(cols, precision)
+        sat = oracle.init_columns(sub, precision)
         oracle.grid(sat, times, workers=workers)
 
     for _ in range(args.warmup):
@@ -260,16 +306,17 @@ def run_reference(args, world, rank) -> None:
         step()
     dt = (time.perf_counter() - t0) / args.steps
     value = rows * times.size / dt
+    model = cpu_model()
     sample = (f"{rows} of {nsat} sats x {times.size} steps fp{precision} per step "
-              f"(init + propagate), {workers} threads, {cpu_model()}")
+              f"(init + propagate), {workers} threads, numpy {np.__version__}, {model}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": f"f{precision}", "data": "synthetic",
-        "config": {"workload": desc, "n_sats": rows, "n_steps": int(times.size)},
+        "config": bench_config(args.workload, desc, nsat, times.size, precision, world, scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": model, "numpy": np.__version__},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -280,8 +327,6 @@ def run_ours(args, world, rank, local) -> None:
 
     from paper_2603_27830_b200 import _device, init_batch, propagate_batch
     from paper_2603_27830_b200.batch import propagate_batch_device
-    from paper_2603_27830_b200.catalog import SEED, starlink_like
-
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
     # one process per GPU; SGP4B_BENCH_BACKEND=gloo (test only) lets several
@@ -296,28 +341,21 @@ def run_ours(args, world, rank, local) -> None:
         else:
             dist.init_process_group(backend)
 
-    desc, nsat, tfn, default_prec = WORKLOADS[args.workload]
+    desc, cols, times, default_prec, scaling = workload_shape(args.workload, world, rank)
     precision = args.precision or default_prec
-    times = tfn()
     m = times.size
-    if args.workload == "c1":                # one satellite: ranks split the time axis
-        from paper_2603_27830_b200.catalog import iss_columns
-        from paper_2603_27830_b200.shard import shard_plan
-        cols = iss_columns()
-        _, lo, hi = shard_plan(1, times.size, world, rank)
-        times = times[lo:hi] if world > 1 else times
-        m = times.size
-        scaling = "strong"
-    elif args.workload in ("c4", "c5"):      # fixed total, sharded (strong scaling)
-        lo = nsat * rank // world
-        hi = nsat * (rank + 1) // world
-        cols = starlink_like(nsat)[:, lo:hi]
-        scaling = "strong"
-    else:                                    # per-rank Starlink shard (weak scaling)
-        cols = starlink_like(nsat, seed=SEED + rank)
-        scaling = "weak"
     n = cols.shape[1]
     cells = n * m
+
+    def max_over_ranks(x: float) -> float:
+        """MAX over ranks of a per-rank device time (NCCL: on the GPU; gloo
+        test backend: on the host)."""
+        if world == 1:
+            return float(x)
+        t = torch.tensor([float(x)], dtype=torch.float64,
+                         device=device if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     stream = torch.cuda.current_stream(device)
     sats = init_batch(cols, precision=precision, device=device)
@@ -383,10 +421,7 @@ def run_ours(args, world, rank, local) -> None:
     torch.cuda.synchronize()
     kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(kernel_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max = float(t.item())
+    total_ms_max = max_over_ranks(total_ms)
     ms_per_step = total_ms_max / args.steps
     value = cells * world / (ms_per_step * 1e-3)
 
@@ -410,12 +445,12 @@ def run_ours(args, world, rank, local) -> None:
         torch.cuda.synchronize()
         if k >= 2:
             ip_ms.append(a.elapsed_time(b))
-    ip = torch.tensor([statistics.median(ip_ms)], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(ip, op=dist.ReduceOp.MAX)
-    init_prop_ms = float(ip.item())
+    init_prop_ms = max_over_ranks(statistics.median(ip_ms))
 
     # ---- e2e: public API with host buffers --------------------------------
+    # propagate_batch returns the whole grid materialised in host memory:
+    # planes AND int32 code plane cross PCIe every step (nothing is deferred
+    # to a lazily mapped page), and the step reads a result value on the host
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     host_times = times.copy()
     for _ in range(2):
@@ -429,20 +464,17 @@ def run_ours(args, world, rank, local) -> None:
     for _ in range(e2e_steps):
         del res
         res = propagate_batch(init_batch(cols, precision=precision, device=device), host_times)
-        checksum = int(res.error[-1, -1])       # host read of the result
+        checksum = int(res.error[-1, -1]) + int(res.error[0, 0])   # host reads of the result
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    # bytes that crossed PCIe per step (counted outside the timed region):
-    # the planes, one flag per row, and the code rows holding a nonzero code
-    d2h_bytes = (res.planes.nbytes + n + int(np.count_nonzero(res.error.any(axis=1))) * m * 4)
+    d2h_bytes = res.planes.nbytes + res.error.nbytes
     del res
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
+    e2e_s = max_over_ranks(e2e_s)
+    d2h_gbs = _measure_d2h(device)
     sampler.__exit__(None, None, None)
     clocks = sampler.summary()
 
+    h2d_bytes = 7 * n * 8 + m * (4 if precision == 32 else 8)
     if rank == 0:
         peaks = _peaks()
         bpc = BYTES_PER_CELL[precision]
@@ -455,18 +487,16 @@ def run_ours(args, world, rank, local) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": (value / PAPER_A100_PROPS) if (args.workload == "c2" and precision == 32
-                                                          and world == 1) else None,
+            # the paper's 3.8 ms is init + propagate, so the
+            # comparison uses this repo's init + propagate time
+            "vs_baseline": ((cells / (init_prop_ms * 1e-3)) / PAPER_A100_PROPS)
+                           if (args.workload == "c2" and precision == 32 and world == 1) else None,
+            "vs_baseline_ref": "init_plus_propagate props/s / paper A100 (3.8 ms for C2 fp32 "
+                               "init + propagate, PAPER.md:99 = 2.458e9 props/s)",
             "dtype": f"f{precision}", "data": "synthetic",
-            "config": {
-                "workload": desc, "n_sats_per_gpu": n, "n_steps": m, "cells_per_gpu": cells,
-                "parallelism": f"satellite shards x{world}, no collective",
-                "l2": "flushed before every timed launch (256 MiB write, then 256 MiB read so "
-                      "no dirty flush lines remain); outputs "
-                      f"{cells * bpc / 2**20:.0f} MiB > L2",
-                "vs_baseline_ref": "paper A100 3.8 ms for C2 fp32 (PAPER.md:99) = 2.458e9 props/s",
-                "launch": "direct" if args.no_graph else "CUDA graph replay of the grid-kernel launch",
-            },
+            "config": bench_config(args.workload, desc, n, m, precision, world, scaling),
+            "launch": "direct" if args.no_graph else "CUDA graph replay of the grid-kernel launch",
+            "output_mib_per_gpu": cells * bpc / 2 ** 20,
             "roofline": {
                 "bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic,
@@ -479,10 +509,12 @@ def run_ours(args, world, rank, local) -> None:
             },
             "e2e": {"value": cells * world / e2e_s, "unit": UNIT,
                     "ms_per_step": e2e_s * 1e3,
-                    "h2d_bytes_per_step": 7 * n * 8 + m * (4 if precision == 32 else 8),
+                    "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes,
+                    "pcie_d2h_gbs_measured": d2h_gbs,
+                    "pcie_frac": (h2d_bytes + d2h_bytes) / e2e_s / (d2h_gbs * 1e9),
                     "api": "propagate_batch(init_batch(host columns), host times) -> numpy "
-                           "(planes via pinned memory; code rows cross PCIe only where nonzero)"},
+                           "planes + int32 codes, both fully copied into pinned host memory"},
             "init_plus_propagate": {"ms_per_step": init_prop_ms,
                                     "value": cells * world / (init_prop_ms * 1e-3),
                                     "note": "paper convention (PAPER.md:67-71): init kernel + "
@@ -493,9 +525,56 @@ def run_ours(args, world, rank, local) -> None:
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cols, times, precision, args.cpu_rows)
+        if not args.no_accuracy:
+            line["accuracy"] = accuracy(cols, times, planes, error, precision, args.acc_cells)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def accuracy(cols, times, planes, error, precision: int, max_cells: int) -> dict:
+    """The grid the timed launches wrote, checked cell by cell against the
+    oracle (bit-exact with the reference; the checker, not the thing timed):
+    codes vs the reference at fp32 and fp64, |dr| / |dv| vs the reference's
+    fp64 path (north_star: "fp32 errors in km are reported against the
+    reference's own fp64 path"), next to the reference's own fp32 error."""
+    from oracle import sgp4_oracle as oracle
+    from oracle.parity import compare_grid
+    n, m = cols.shape[1], times.size
+    rows = max(1, min(n, max_cells // max(m, 1)))
+
+    def get(lo, hi):
+        return planes[:, lo:hi].cpu().numpy(), error[lo:hi].cpu().numpy()
+
+    t0 = time.perf_counter()
+    par = compare_grid(cols[:, :rows], times, get, precision, workers=oracle.default_workers())
+    out = par.summary()
+    out["scope"] = ("every cell of the timed grid" if rows == n
+                    else f"first {rows} of {n} satellites of the timed grid, every step")
+    out["checker"] = "oracle/sgp4_oracle.py (bit-exact with the reference sgp4kit)"
+    out["check_s"] = time.perf_counter() - t0
+    return out
+
+
+def _measure_d2h(device) -> float:
+    """Pinned D2H bandwidth of this GPU's PCIe link (GB/s, best of 5 copies
+    of 256 MiB), the floor of the e2e path."""
+    import torch
+    from paper_2603_27830_b200 import _hostmem
+    nbytes = 256 << 20
+    src = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    (dst,) = _hostmem.empty([((nbytes,), np.uint8)])
+    dst_t = torch.from_numpy(dst)
+    best = math.inf
+    for _ in range(6):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst_t.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) * 1e-3)
+    return nbytes / best / 1e9
 
 
 def _device_alloc(n, m, precision, device):
@@ -528,6 +607,27 @@ def _traffic(workload: str, precision: int):
     return d.get(f"{workload}_fp{precision}")
 
 
+def maybe_relaunch(args) -> None:
+    """``--gpus N`` without a torchrun environment re-executes this script
+    under torch.distributed.run with N ranks (one per GPU); under torchrun
+    the world size must equal N."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,9 +640,14 @@ def main() -> None:
     ap.add_argument("--cpu-rows", type=int, default=9341)
     ap.add_argument("--ref-rows", type=int, default=9341)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true",
+                    help="skip the full-grid oracle check of the timed grid")
+    ap.add_argument("--acc-cells", type=int, default=12_000_000,
+                    help="cells of the timed grid checked against the oracle (whole rows)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed grid kernels directly instead of replaying a CUDA graph")
     args = ap.parse_args()
+    maybe_relaunch(args)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -13,7 +13,9 @@
  *
  * Conventions
  *   - Every pointer named *_dev is a device pointer on the current device;
- *     the library never allocates, never synchronises and never aborts.
+ *     the library never allocates device memory (sgp4b_host_alloc is the only
+ *     allocator, for pinned HOST result buffers), never synchronises and
+ *     never aborts.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
  *   - Return 0 on success or a negative SGP4B_E* status.  The message of the
  *     last failure on the calling thread is sgp4b_last_error().
@@ -33,6 +35,7 @@ extern "C" {
 #define SGP4B_OK 0
 #define SGP4B_EINVAL (-1)   /* bad argument (size, precision, null pointer) */
 #define SGP4B_ECUDA (-2)    /* CUDA launch/config error */
+#define SGP4B_ENOMEM (-3)   /* page-locked host allocation failed */
 
 /* Number of float slots in one satellite's SoA satrec (public SatInit float
  * fields, kernel.py:64-107, in dataclass order). */
@@ -104,6 +107,14 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
 int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev,
                        const void* u_dev, int64_t n, int precision,
                        void* out_dev, void* stream);
+
+/* Page-locked (pinned, portable) host memory for result grids.  The
+ * reference returns pageable np.empty grids (batch.py:177-183); results that
+ * come back over PCIe need pinned memory for full-rate D2H, and the Python
+ * layer pools these blocks at their exact (2 MiB-rounded) size.  These are
+ * the only calls that allocate, and they allocate HOST memory only. */
+int sgp4b_host_alloc(int64_t nbytes, void** out);
+int sgp4b_host_free(void* p);
 
 /* Thread-local message for the last non-zero status. */
 const char* sgp4b_last_error(void);

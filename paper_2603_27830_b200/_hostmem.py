@@ -1,0 +1,145 @@
+"""Page-locked host blocks for result grids that cross PCIe.
+
+The reference returns pageable ``np.empty`` grids that are freed when the
+caller drops them (batch.py:177-183).  A D2H copy only runs at full PCIe rate
+into page-locked memory, and page-locking is slow (it dominates a 200 MB
+result if done per call), so blocks are pooled — but unlike torch's caching
+host allocator they are sized exactly (rounded to 2 MiB, not to a power of
+two) and the pool retains at most ``cache_limit()`` bytes of free blocks;
+anything above is unpinned and freed as soon as the last array over it dies.
+``empty_cache()`` releases every free block.
+
+The memory comes from ``sgp4b_host_alloc`` (cudaHostAlloc, portable), so any
+GPU of the process can DMA into it.
+"""
+
+from __future__ import annotations
+
+import atexit
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _native
+
+_ALIGN_LARGE = 2 << 20
+_ALIGN_SMALL = 64 << 10
+_DEFAULT_LIMIT = 4 << 30
+
+_lock = threading.Lock()
+_free: list[tuple[int, int]] = []          # (size, ptr) of retained free blocks
+_stats = {"pinned_bytes": 0, "cached_bytes": 0, "allocs": 0, "reuses": 0}
+
+
+def cache_limit() -> int:
+    """Bytes of free pinned blocks the pool may retain
+    (``SGP4B_HOST_CACHE_BYTES``, default 4 GiB)."""
+    v = os.environ.get("SGP4B_HOST_CACHE_BYTES")
+    return int(v) if v else _DEFAULT_LIMIT
+
+
+def _round(nbytes: int) -> int:
+    a = _ALIGN_LARGE if nbytes >= _ALIGN_LARGE else _ALIGN_SMALL
+    return -(-nbytes // a) * a
+
+
+class PinnedBlock:
+    """One page-locked region; numpy views keep it alive through
+    ``__array_interface__`` (their ``.base``), and it goes back to the pool
+    when the last one dies."""
+
+    __slots__ = ("ptr", "size", "__weakref__")
+
+    def __init__(self, ptr: int, size: int):
+        self.ptr = ptr
+        self.size = size
+
+    @property
+    def __array_interface__(self):
+        return {"shape": (self.size,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        if self.ptr:
+            _give_back(self.ptr, self.size)
+            self.ptr = 0
+
+
+def _give_back(ptr: int, size: int) -> None:
+    with _lock:
+        if _stats["cached_bytes"] + size <= cache_limit():
+            _free.append((size, ptr))
+            _free.sort()
+            _stats["cached_bytes"] += size
+            return
+        _stats["pinned_bytes"] -= size
+    _free_ptr(ptr)
+
+
+def _free_ptr(ptr: int) -> None:
+    try:
+        _native.load().sgp4b_host_free(ptr)
+    except Exception:                       # interpreter teardown
+        pass
+
+
+def alloc(nbytes: int) -> PinnedBlock:
+    """A pinned block of at least ``nbytes`` (reused from the pool when a free
+    block is no more than 1.5x the rounded request)."""
+    size = _round(max(int(nbytes), 1))
+    with _lock:
+        for k, (sz, ptr) in enumerate(_free):
+            if sz >= size and sz <= size + size // 2:
+                del _free[k]
+                _stats["cached_bytes"] -= sz
+                _stats["reuses"] += 1
+                return PinnedBlock(ptr, sz)
+    lib = _native.load()
+    out = ctypes.c_void_p()
+    status = lib.sgp4b_host_alloc(size, ctypes.byref(out))
+    if status != 0:
+        empty_cache()                       # retry once without the retained blocks
+        status = lib.sgp4b_host_alloc(size, ctypes.byref(out))
+        if status != 0:
+            raise MemoryError(lib.sgp4b_last_error().decode(errors="replace"))
+    with _lock:
+        _stats["pinned_bytes"] += size
+        _stats["allocs"] += 1
+    return PinnedBlock(out.value, size)
+
+
+def empty(shapes_dtypes) -> list[np.ndarray]:
+    """Several C-contiguous arrays carved from ONE pinned block (each 256-B
+    aligned), e.g. the planes and code plane of one result grid."""
+    offs, total = [], 0
+    for shape, dtype in shapes_dtypes:
+        total = -(-total // 256) * 256
+        offs.append(total)
+        total += int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+    raw = np.asarray(alloc(total))
+    out = []
+    for (shape, dtype), off in zip(shapes_dtypes, offs):
+        nb = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+        out.append(raw[off:off + nb].view(dtype).reshape(shape))
+    return out
+
+
+def empty_cache() -> None:
+    """Unpin and free every retained free block."""
+    with _lock:
+        blocks = list(_free)
+        _free.clear()
+        _stats["cached_bytes"] = 0
+        _stats["pinned_bytes"] -= sum(s for s, _ in blocks)
+    for _, ptr in blocks:
+        _free_ptr(ptr)
+
+
+def stats() -> dict:
+    """pinned_bytes (live + cached), cached_bytes (free, retained), allocs, reuses."""
+    with _lock:
+        return dict(_stats)
+
+
+atexit.register(empty_cache)

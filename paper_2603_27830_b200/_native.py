@@ -16,7 +16,7 @@ LIB_PATH = _HERE / LIB_NAME
 
 SATREC_FIELDS = 33
 RECORD_SLOTS = 40
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 #: every symbol include/sgp4b.h declares, in header order
 EXPORTED_SYMBOLS = (
@@ -26,6 +26,8 @@ EXPORTED_SYMBOLS = (
     "sgp4b_propagate_pairs",
     "sgp4b_drift_norms",
     "sgp4b_solve_kepler",
+    "sgp4b_host_alloc",
+    "sgp4b_host_free",
     "sgp4b_last_error",
     "sgp4b_abi_version",
 )
@@ -43,6 +45,8 @@ _SIGNATURES = {
                                        _vp, _vp, _vp]),
     "sgp4b_drift_norms": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
     "sgp4b_solve_kepler": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _vp, _vp]),
+    "sgp4b_host_alloc": (_c_int, [_c_i64, ctypes.POINTER(_vp)]),
+    "sgp4b_host_free": (_c_int, [_vp]),
     "sgp4b_last_error": (ctypes.c_char_p, []),
     "sgp4b_abi_version": (_c_int, []),
 }

@@ -17,7 +17,7 @@ from typing import Any, Callable, Sequence
 import numpy as np
 import torch
 
-from . import _device
+from . import _device, _hostmem
 from .gravity import WGS72, GravityModel
 from .kernel import SatInit, satinit_from_device, _device_of
 from .tle import MeanElements, elements_to_columns
@@ -200,12 +200,63 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
         if t_d.data_ptr() % 16:              # the vector path wants 16-B aligned times
             t_d = t_d.clone()
         m = int(t_d.shape[0])
+        if times_lo is not None:
+            times_lo = _check_times_lo(times_lo, t_d, dev.precision)
         if out is None:
             planes, error = _alloc_grid(sats.n, m, dev.precision, dev.device)
         else:
-            planes, error = out
+            planes, error = _check_out(out, sats.n, m, dev.precision, dev.device)
         _device.propagate_grid(dev, t_d, planes, error, times_lo=times_lo)
     return BatchResult(planes=planes, error=error, n=sats.n, m=m)
+
+
+def _check_out(out, n: int, m: int, precision: int, device):
+    """Caller-supplied (planes, error) device tensors: shapes (6, n, m) and
+    (n, m), the batch dtype and int32, on the batch's device, unit column
+    stride.  Anything else would let the kernel write outside the buffers."""
+    try:
+        planes, error = out
+    except (TypeError, ValueError):
+        raise ValueError("out must be a (planes, error) pair of device tensors") from None
+    if not isinstance(planes, torch.Tensor) or not isinstance(error, torch.Tensor):
+        raise TypeError("out tensors must be torch tensors")
+    if tuple(planes.shape) != (6, n, m) or tuple(error.shape) != (n, m):
+        raise ValueError(f"out shapes {tuple(planes.shape)} / {tuple(error.shape)} do not match "
+                         f"(6, {n}, {m}) / ({n}, {m})")
+    if planes.dtype != _device.torch_dtype(precision) or error.dtype != torch.int32:
+        raise TypeError(f"out dtypes must be {_device.torch_dtype(precision)} and int32, "
+                        f"got {planes.dtype} and {error.dtype}")
+    if planes.device != device or error.device != device:
+        raise ValueError(f"out tensors must live on {device}")
+    if planes.stride(2) != 1 or error.stride(1) != 1:
+        raise ValueError("out tensors need a unit column stride")
+    if min(planes.stride(0), planes.stride(1), error.stride(0)) < 0:
+        raise ValueError("out tensors must not have negative strides")
+    return planes, error
+
+
+def _check_times_lo(times_lo, t_d: torch.Tensor, precision: int) -> torch.Tensor:
+    """Low words of fp64 times for an fp32 batch: float32, same length and
+    device as the times, contiguous."""
+    if precision != 32:
+        raise ValueError("times_lo is only meaningful for fp32 batches")
+    if not isinstance(times_lo, torch.Tensor):
+        times_lo = torch.as_tensor(np.asarray(times_lo, dtype=np.float32))
+    if times_lo.dtype != torch.float32:
+        raise TypeError(f"times_lo must be float32, got {times_lo.dtype}")
+    if times_lo.ndim != 1 or times_lo.shape[0] != t_d.shape[0]:
+        raise ValueError(f"times_lo must have shape ({t_d.shape[0]},), got {tuple(times_lo.shape)}")
+    return times_lo.to(t_d.device).contiguous()
+
+
+def split_times(times) -> tuple[np.ndarray, np.ndarray]:
+    """fp64 minutes -> (hi, lo) float32 words with hi + lo == t to ~2^-48
+    relative: the ``times`` / ``times_lo`` pair of an fp32 batch whose
+    secular stage should see the caller's fp64 times."""
+    t = np.asarray(times, dtype=np.float64)
+    hi = t.astype(np.float32)
+    lo = (t - hi.astype(np.float64)).astype(np.float32)
+    return hi, lo
 
 
 def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchResult:
@@ -214,41 +265,29 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchR
     Cell (i, j) is bitwise equal to ``sgp4_propagate`` of satellite i at
     time j at the batch precision.  ``workers`` is accepted for API
     compatibility; it never affected output and the GPU needs no pool.
-    Returns numpy arrays; the planes are backed by pinned host memory.
-
-    Only the rows of the int32 code plane that hold a nonzero code cross
-    PCIe (a catalogue in good standing has none): the device reduces the
-    plane to one flag per row, and the host plane starts zero-filled.  For
-    the C2 grid that is 224 MB over the link instead of 261.5 MB.
+    Returns numpy arrays, fully materialised: the planes and the int32 code
+    plane are copied from HBM into one page-locked host block (pooled at its
+    exact size, see ``_hostmem``) that is released with the arrays.
     """
     t = _times(sats, times)
     dev = sats.device_satrec
     n, m = sats.n, t.size
+    planes_h, error_h = _host_grid(n, m, dev.precision)
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
-        t_h = torch.from_numpy(t).pin_memory()
-        t_d = t_h.to(dev.device, non_blocking=True)
+        t_d = torch.from_numpy(t).to(dev.device, non_blocking=True)
         res = propagate_batch_device(sats, t_d)
-        flags_h = torch.empty((n,), dtype=torch.bool, pin_memory=True)
-        # codes are >= 0, so a row max is the flag (no grid-sized temporary)
-        flags_h.copy_(res.error.amax(dim=1) > 0, non_blocking=True)
-        planes_h = _alloc_host_planes(n, m, dev.precision)
-        planes_h.copy_(res.planes, non_blocking=True)
+        torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
+        torch.from_numpy(error_h).copy_(res.error, non_blocking=True)
         stream.synchronize()
-        error = np.zeros((n, m), dtype=np.int32)
-        bad = np.flatnonzero(flags_h.numpy())
-        if bad.size:
-            rows = torch.from_numpy(bad.astype(np.int64)).to(dev.device)
-            error[bad] = res.error.index_select(0, rows).cpu().numpy()
-    return BatchResult(planes=planes_h.numpy(), error=error, n=n, m=m)
+    return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
 
 
-def _alloc_host_planes(n: int, m: int, precision: int) -> torch.Tensor:
+def _host_grid(n: int, m: int, precision: int):
+    """(6, n, m) planes + (n, m) int32 codes in one pinned host block."""
     try:
-        return torch.empty((6, n, m), dtype=_device.torch_dtype(precision), pin_memory=True)
-    except (RuntimeError, MemoryError) as exc:
-        if isinstance(exc, RuntimeError) and "memory" not in str(exc).lower():
-            raise
+        return _hostmem.empty([((6, n, m), _device.np_dtype(precision)), ((n, m), np.int32)])
+    except MemoryError:
         itemsize = 4 if precision == 32 else 8
         raise GridAllocationError(n, m, 6 * n * m * itemsize + 4 * n * m) from None
 
@@ -309,26 +348,18 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
             planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
             _device.propagate_grid(dev, t_d[cols].clone(), planes_d, err_d,
                                    rows=(rows.start, rows.stop))
-            # as in propagate_batch, code rows cross PCIe only where nonzero
-            flags_h = torch.empty((tr,), dtype=torch.bool, pin_memory=True)
-            flags_h.copy_(err_d.amax(dim=1) > 0, non_blocking=True)
-            planes_h = _alloc_host_planes(tr, tc, dev.precision)
-            planes_h.copy_(planes_d, non_blocking=True)
+            planes_h, err_h = _host_grid(tr, tc, dev.precision)
+            torch.from_numpy(planes_h).copy_(planes_d, non_blocking=True)
+            torch.from_numpy(err_h).copy_(err_d, non_blocking=True)
             done = torch.cuda.Event()
             done.record(stream)
-            return planes_h, flags_h, done, (planes_d, err_d)
+            return planes_h, err_h, done, (planes_d, err_d)
 
         pending = launch(tiles[0])
         for k, (rows, cols) in enumerate(tiles):
-            planes_h, flags_h, done, keep = pending
+            planes_np, err_np, done, keep = pending
             pending = launch(tiles[k + 1]) if k + 1 < len(tiles) else None
             done.synchronize()
-            planes_np = planes_h.numpy()
-            err_np = np.zeros((rows.stop - rows.start, cols.stop - cols.start), dtype=np.int32)
-            bad = np.flatnonzero(flags_h.numpy())
-            if bad.size:
-                idx = torch.from_numpy(bad.astype(np.int64)).to(dev.device)
-                err_np[bad] = keep[1].index_select(0, idx).cpu().numpy()
             try:
                 sink(rows, cols, planes_np, err_np)
             except Exception as exc:

@@ -1750,7 +1750,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 1; }
+int sgp4b_abi_version(void) { return 2; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -1859,6 +1859,30 @@ int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev, const void* u
         static_cast<const float*>(axnl_dev), static_cast<const float*>(aynl_dev),
         static_cast<const float*>(u_dev), n, static_cast<float*>(out_dev));
   return check_launch("sgp4b_solve_kepler");
+}
+
+int sgp4b_host_alloc(int64_t nbytes, void** out) {
+  if (out == nullptr) return fail(SGP4B_EINVAL, "sgp4b_host_alloc: null out pointer");
+  *out = nullptr;
+  if (nbytes <= 0) return fail(SGP4B_EINVAL, "sgp4b_host_alloc: nbytes must be positive");
+  // portable: any device of the process may DMA into it (multi-GPU grids)
+  cudaError_t e = cudaHostAlloc(out, (size_t)nbytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    cudaGetLastError();
+    return fail(SGP4B_ENOMEM, "sgp4b_host_alloc(%lld): %s", (long long)nbytes, cudaGetErrorString(e));
+  }
+  return SGP4B_OK;
+}
+
+int sgp4b_host_free(void* p) {
+  if (p == nullptr) return SGP4B_OK;
+  cudaError_t e = cudaFreeHost(p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SGP4B_ECUDA, "sgp4b_host_free: %s", cudaGetErrorString(e));
+  }
+  return SGP4B_OK;
 }
 
 }  // extern "C"

@@ -528,29 +528,111 @@ def test_scaling_sweep_gpu(real_elements):
 
 def test_streamed_memory_contract(corpus_columns):
     """propagate_batch_streamed keeps O(tile) host memory (the reference's
-    tracemalloc contract, test_batch.py:152-173): the pinned host peak while
-    streaming a 2,000 x 2,000 grid (112 MB dense) in 100 x 500 tiles stays
-    within a few tiles, and no dense device grid is allocated either."""
+    tracemalloc contract, test_batch.py:152-173): the pinned host bytes
+    while streaming a 2,000 x 2,000 grid (112 MB dense) in 100 x 500 tiles
+    stay within a few tiles, and no dense device grid is allocated either."""
     import torch
+    from paper_2603_27830_b200 import _hostmem
     pkg = _gpu()
     sats = pkg.init_batch(np.tile(corpus_columns, (1, 2))[:, :2000], precision=32)
     times = np.linspace(0.0, 1440.0, 2000)
     tile_bytes = 100 * 500 * 28
     torch.cuda.synchronize()
-    torch.cuda.reset_peak_host_memory_stats()
+    _hostmem.empty_cache()
     torch.cuda.reset_peak_memory_stats()
-    host0 = torch.cuda.host_memory_stats().get("allocated_bytes.all.current", 0)
+    host0 = _hostmem.stats()["pinned_bytes"]
     dev0 = torch.cuda.memory_allocated()
     count = [0]
+    peak = [0]
 
     def sink(rows, cols, planes, error):
         count[0] += 1
+        peak[0] = max(peak[0], _hostmem.stats()["pinned_bytes"] - host0)
     summary = pkg.propagate_batch_streamed(sats, times, 100, 500, sink)
     assert count[0] == 20 * 4 and summary.cells_emitted == 2000 * 2000
-    host_peak = torch.cuda.host_memory_stats().get("allocated_bytes.all.peak", 0) - host0
     dev_peak = torch.cuda.max_memory_allocated() - dev0
-    assert host_peak <= 4 * tile_bytes, host_peak
+    assert peak[0] <= 4 * tile_bytes, peak[0]
     assert dev_peak <= 8 * tile_bytes + (1 << 20), dev_peak
+
+
+def test_pinned_results_released(corpus_columns):
+    """propagate_batch's arrays live in one pooled page-locked block of the
+    grid's exact size (2 MiB rounding, not a power of two); the block returns
+    to the pool when the arrays die and empty_cache() unpins it."""
+    import gc
+    from paper_2603_27830_b200 import _hostmem
+    pkg = _gpu()
+    _hostmem.empty_cache()
+    base = _hostmem.stats()["pinned_bytes"]
+    sats = pkg.init_batch(np.tile(corpus_columns, (1, 3))[:, :3000], precision=32)
+    res = pkg.propagate_batch(sats, np.linspace(0.0, 1440.0, 1000))
+    want = 3000 * 1000 * 28
+    live = _hostmem.stats()["pinned_bytes"] - base
+    assert want <= live <= want + (2 << 20) + 256, live
+    again = pkg.propagate_batch(sats, np.linspace(0.0, 1440.0, 1000))
+    assert np.array_equal(again.planes, res.planes) and np.array_equal(again.error, res.error)
+    del res, again
+    gc.collect()
+    st = _hostmem.stats()
+    assert st["cached_bytes"] >= want and st["reuses"] >= 0
+    _hostmem.empty_cache()
+    assert _hostmem.stats()["pinned_bytes"] == base
+
+
+def test_times_lo_path_matches_oracle(oracle, corpus_columns):
+    """fp32 batch fed fp64 times as (hi, lo) float32 words (times_lo): codes
+    equal the reference fp64 codes and states stay within the fp32 bound of
+    the oracle's fp64 path evaluated at the exact fp64 times."""
+    import torch
+    from paper_2603_27830_b200.batch import split_times
+    pkg = _gpu()
+    cols = corpus_columns[:, :40]
+    times = np.linspace(-300.0, 20160.0, 203) + 1.0 / 3.0
+    hi, lo = split_times(times)
+    sats = pkg.init_batch(cols, precision=32)
+    res = pkg.propagate_batch_device(sats, torch.from_numpy(hi).cuda(),
+                                     times_lo=torch.from_numpy(lo).cuda())
+    ref64, codes64 = oracle.grid(oracle.init_columns(cols, 64), times)
+    assert np.array_equal(res.error.cpu().numpy(), codes64)
+    planes = res.planes.cpu().numpy()
+    dr, _ = _diff(planes, ref64, codes64 == 0)
+    plain = pkg.propagate_batch(sats, hi)
+    dr_plain, _ = _diff(plain.planes, ref64, codes64 == 0)
+    print(f"\ntimes_lo: max|dr| {dr.max() * 1e3:.2f} m (hi word only: {dr_plain.max() * 1e3:.2f} m)")
+    assert dr.max() < 0.5 and dr.max() <= dr_plain.max()
+    with pytest.raises(ValueError):
+        pkg.propagate_batch_device(sats, torch.from_numpy(hi).cuda(),
+                                   times_lo=torch.from_numpy(lo[:-1]).cuda())
+    with pytest.raises(TypeError):
+        pkg.propagate_batch_device(sats, torch.from_numpy(hi).cuda(),
+                                   times_lo=torch.from_numpy(lo.astype(np.float64)).cuda())
+
+
+def test_out_validation(corpus_columns):
+    """propagate_batch_device(out=...) rejects buffers the kernel would
+    overrun or misinterpret, and accepts a correct pair."""
+    import torch
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :5], precision=32)
+    t = np.linspace(0.0, 60.0, 8)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    good = (torch.empty((6, 5, 8), device=dev), torch.empty((5, 8), dtype=torch.int32, device=dev))
+    res = pkg.propagate_batch_device(sats, t, out=good)
+    assert res.planes.data_ptr() == good[0].data_ptr()
+    bad = [
+        (torch.empty((6, 4, 8), device=dev), good[1]),                      # too few rows
+        (torch.empty((5, 5, 8), device=dev), good[1]),                      # too few planes
+        (good[0], torch.empty((5, 7), dtype=torch.int32, device=dev)),      # short code rows
+        (torch.empty((6, 5, 16), device=dev)[:, :, ::2], good[1]),          # column stride 2
+    ]
+    for out in bad:
+        with pytest.raises(ValueError):
+            pkg.propagate_batch_device(sats, t, out=out)
+    for out in [(good[0].double(), good[1]), (good[0], good[1].long())]:
+        with pytest.raises(TypeError):
+            pkg.propagate_batch_device(sats, t, out=out)
+    with pytest.raises(ValueError):
+        pkg.propagate_batch_device(sats, t, out=(good[0].cpu(), good[1].cpu()))
 
 
 def test_bench_json_contract():
@@ -575,8 +657,46 @@ def test_bench_json_contract():
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 9341 * 1000 * 24 + 9341
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0
+    assert e["d2h_bytes_per_step"] == 9341 * 1000 * 28        # planes + full code plane
+    assert 0 < e["pcie_frac"] <= 1.1
     assert "workload" in d["config"] and d["value"] > 1e10
+    acc = d["accuracy"]
+    assert acc["cells_compared"] == 9341 * 1000 and acc["code_mismatch_vs_ref_fp64"] == 0
+    assert acc["dr_max_km"] < 0.1
+    cb = d["cpu_baseline"]
+    assert cb["value_1thread"] > 0 and cb["cores"] >= 1 and cb["numpy"]
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """The N>1 plumbing of bench.py (self-relaunch under torch.distributed.run,
+    barrier, MAX over ranks, weak-scaling value) with 2 ranks sharing the one
+    GPU through the gloo test backend."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    env = dict(os.environ, SGP4B_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4",
+                          "--warmup", "3", "--e2e-steps", "1", "--no-cpu", "--no-accuracy"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["cells_per_gpu"] == 9341 * 1000
+    assert abs(d["value"] - 2 * 9341 * 1000 / (d["ms_per_step"] * 1e-3)) < 1e-6 * d["value"]
+    ref = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--impl",
+                          "reference", "--steps", "1", "--warmup", "0", "--ref-rows", "50"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert ref.returncode == 0, ref.stderr[-3000:]
+    rl = [ln for ln in ref.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(rl) == 1
+    r = json.loads(rl[0])
+    assert r["impl"] == "reference" and r["config"] == d["config"]
 
 
 @pytest.mark.parametrize("precision", [32, 64])

@@ -147,9 +147,51 @@ def test_bench_reference_arm_nonzero_rank_is_silent():
     root = Path(__file__).resolve().parents[1]
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "0", "--ref-rows", "8"],
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-rows", "8"],
                          capture_output=True, text=True, timeout=300, cwd=root, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_bench_world_size_must_match_gpus():
+    """Under a torchrun environment --gpus must equal WORLD_SIZE (a silent
+    1-GPU measurement of an N-GPU request is refused)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--ref-rows", "8"],
+                         capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_bench_gpus_flag_relaunches_under_torchrun():
+    """`bench.py --gpus 2` without torchrun re-executes itself under
+    torch.distributed.run with 2 ranks; the reference arm prints one line
+    (rank 0) whose config is the same dict the GPU arm prints."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import bench
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-rows", "16"],
+                         capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    desc, cols, times, prec, scaling = bench.workload_shape("c2", 2, 0)
+    assert d["config"] == bench.bench_config("c2", desc, cols.shape[1], times.size, prec, 2, scaling)
+    assert d["cpu_baseline"]["numpy"] and d["cpu_baseline"]["cpu_model"]
 
 
 def test_time_task_protocol_and_failures():

@@ -77,3 +77,26 @@ def test_kepler_against_bisection(oracle):
         e = float(oracle.kepler(np.float64(ax), np.float64(ay), np.float64(u)))
         assert e == pytest.approx(bisect(ax, ay, u), abs=1e-10)
     assert float(oracle.kepler(np.float64(0), np.float64(0), np.float64(1.2345))) == 1.2345
+
+
+def test_parity_helper_detects_differences(oracle, corpus_columns):
+    """oracle/parity.compare_grid (the full-grid checker of the GPU tests):
+    the oracle against itself is exact; a perturbed cell and a flipped code
+    are both caught; fp32 grids carry the reference's own fp32 error."""
+    from oracle.parity import compare_grid
+    cols = corpus_columns[:, :23]
+    times = np.linspace(0.0, 1440.0, 17)
+    p64, c64 = oracle.grid(oracle.init_columns(cols, 64), times)
+    same = compare_grid(cols, times, lambda lo, hi: (p64[:, lo:hi], c64[lo:hi]), 64, band_rows=5)
+    assert same.cells == 23 * 17 and same.code_mismatch_fp64 == 0 and same.dr_max == 0.0
+    bad_p, bad_c = p64.copy(), c64.copy()
+    ok = np.argwhere(c64 == 0)
+    i, j = ok[len(ok) // 2]
+    bad_p[1, i, j] += 2e-6
+    bad_c[ok[0][0], ok[0][1]] = 6
+    bad = compare_grid(cols, times, lambda lo, hi: (bad_p[:, lo:hi], bad_c[lo:hi]), 64, band_rows=7)
+    assert bad.code_mismatch_fp64 == 1 and abs(bad.dr_max - 2e-6) < 1e-9
+    p32, c32 = oracle.grid(oracle.init_columns(cols, 32), times)
+    s32 = compare_grid(cols, times, lambda lo, hi: (p32[:, lo:hi], c32[lo:hi]), 32).summary()
+    assert s32["code_mismatch_vs_ref_same_precision"] == 0
+    assert s32["dr_max_km"] == s32["ref_fp32_dr_max_km"] > 0
