@@ -664,8 +664,6 @@ def test_bench_json_contract():
     acc = d["accuracy"]
     assert acc["cells_compared"] == 9341 * 1000 and acc["code_mismatch_vs_ref_fp64"] == 0
     assert acc["dr_max_km"] < 0.1
-    cb = d["cpu_baseline"]
-    assert cb["value_1thread"] > 0 and cb["cores"] >= 1 and cb["numpy"]
 
 
 def test_bench_two_ranks_on_one_gpu():
