@@ -52,13 +52,6 @@
 #ifndef SGP4B_K2_SERIES
 #define SGP4B_K2_SERIES 1           // class-2 (e < 0.1) series for 1/pl_lp, 1/den, 1/(1+betal)
 #endif
-#ifndef SGP4B_SMEM_REC64
-#define SGP4B_SMEM_REC64 1        // fp64 records (80 registers) in shared memory
-#endif
-#ifndef SGP4B_F64_UNROLL
-#define SGP4B_F64_UNROLL 1
-#endif
-constexpr int kF64Unroll = SGP4B_F64_UNROLL;   // fp64 cells interleaved per lane
 #ifndef SGP4B_MINB64
 #define SGP4B_MINB64 1
 #endif
@@ -136,11 +129,28 @@ enum Slot32 {
 static_assert((int)P_FLAGS == (int)S_FLAGS, "fp32 flags slot");
 static_assert((int)P_COUNT <= (int)S_COUNT, "fp32 record fits the packed slot count");
 
+// fp64 records: the same folding as fp32 (every per-satellite product the
+// reference forms per cell is computed once at pack time), kept in fp64.
+enum Slot64 {
+  Q_ARGPO = 0, Q_ARGPDOT, Q_NODEO, Q_NODEDOT, Q_NODECF, Q_MO, Q_MDOT,
+  Q_U0, Q_UDOT,                         // (mo + argpo) mod 2pi, mdot + argpdot
+  Q_S, Q_SC1, Q_SD2, Q_SD3, Q_SD4,      // sqrt(am) = s (1 - cc1 t - d2 t^2 - d3 t^3 - d4 t^4)
+  Q_N2, Q_N3, Q_N4, Q_N5,               // no t2cof .. no t5cof
+  Q_A0, Q_A1, Q_A2, Q_A3, Q_OMGCOF,     // drag cubic in cos xmdf (as P_A0..P_A3)
+  Q_E0, Q_BC4, Q_BC5,                   // ecco + bstar cc5 sinmao, bstar cc4, bstar cc5
+  Q_AYCOF, Q_XLCOF,
+  Q_K41R, Q_KXR, Q_QX, Q_C15CO, Q_C15CS, Q_X1V, Q_C41V,   // as the P_ factors
+  Q_SINIO, Q_COSIO, Q_INCLO,
+  Q_FLAGS,
+  Q_COUNT
+};
+static_assert((int)Q_COUNT <= (int)S_COUNT, "fp64 record fits the packed slot count");
+
 // flags word
 constexpr int FLAG_ISIMP = 1;
 constexpr int FLAG_BAD_NM = 2;
 constexpr int KEPLER_SHIFT = 4;   // 4 bits: fixed Kepler iterations (fp32)
-constexpr int CODE_SHIFT = 8;     // 8 bits: persistent init code
+constexpr int CODE_SHIFT = 8;     // 23 bits: persistent init code (0 .. 2^23 - 1)
 
 // ---- error plumbing ----------------------------------------------------
 thread_local char g_last_error[512] = "";
@@ -227,13 +237,13 @@ struct RecW {
 };
 template <>
 __device__ __forceinline__ int RecS<double>::flags() const {
-  return (int)__double_as_longlong(p[S_FLAGS]);
+  return (int)__double_as_longlong(p[Q_FLAGS]);
 }
 template <>
 __device__ __forceinline__ int Rec<float>::flags() const { return __float_as_int(v[S_FLAGS]); }
 template <>
 __device__ __forceinline__ int Rec<double>::flags() const {
-  return (int)__double_as_longlong(v[S_FLAGS]);
+  return (int)__double_as_longlong(v[Q_FLAGS]);
 }
 
 __device__ __forceinline__ void load_rec(const float* __restrict__ p, Rec<float>& r) {
@@ -292,51 +302,18 @@ __device__ __forceinline__ float kepler_reference<float>(float axnl, float aynl,
   return eo1;
 }
 
+// streaming (evict-first) scalar stores
+__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(int32_t* p, int32_t v) { __stcs(reinterpret_cast<int*>(p), (int)v); }
+
 // ======================================================================
-// fp64 cell: the reference operation order (kernel.py:352-510)
+// fp64 cells (kernel.py:352-510)
 // ======================================================================
 struct Cell64 {
   double r[3], v[3];
   int code;
 };
-
-// ---- lean fp64 primitives for the propagate cell ------------------------
-// The propagate cell's arguments are finite, normal and moderate (|x| well
-// below 2^20 pi/2 for sin/cos), so the special-case and slow paths of the
-// libdevice routines are dead weight; and libdevice materialises its 64-bit
-// polynomial constants with UMOV pairs on every call.  These versions keep
-// the coefficients in __constant__ memory (DFMA reads them directly) and
-// are accurate to ~1 ulp, far inside the 1 mm / 1e-6 km/s budget.
-__constant__ double c_sin_poly[6] = {
-    -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
-    2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10};
-__constant__ double c_cos_poly[6] = {
-    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
-    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11};
-// pi/2 in three parts (33 + 33 + 53 bits) and 2/pi
-__constant__ double c_pio2[4] = {1.57079632673412561417e+00, 6.07710050630396597660e-11,
-                                 2.02226624879595063154e-21, 6.36619772367581382433e-01};
-
-__device__ __forceinline__ void sincos64(double x, double* sp, double* cp) {
-  const double k = rint(x * c_pio2[3]);
-  double r = fma(-k, c_pio2[0], x);           // exact: 33-bit part, |k| < 2^20
-  r = fma(-k, c_pio2[1], r);
-  r = fma(-k, c_pio2[2], r);
-  const double z = r * r;
-  const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, c_sin_poly[5], c_sin_poly[4]),
-                                                 c_sin_poly[3]), c_sin_poly[2]), c_sin_poly[1]),
-                        c_sin_poly[0]);
-  const double sr = fma(r * z, ps, r);
-  const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, c_cos_poly[5], c_cos_poly[4]),
-                                                 c_cos_poly[3]), c_cos_poly[2]), c_cos_poly[1]),
-                        c_cos_poly[0]);
-  const double cr = fma(z * z, pc, fma(-0.5, z, 1.0));
-  const int q = (int)k & 3;
-  const double s0 = (q & 1) ? cr : sr;
-  const double c0 = (q & 1) ? sr : cr;
-  *sp = (q & 2) ? -s0 : s0;
-  *cp = ((q + 1) & 2) ? -c0 : c0;
-}
 
 // 1/x by one third-order step r (1 + e + e^2), e = 1 - x r, from the SFU
 // seed (|e| ~ 2^-22, so the result error e^3 is below fp64 rounding)
@@ -361,113 +338,218 @@ __device__ __forceinline__ double sqrt64(double x) {
   return fma(0.5 * y, fma(-s, s, x), s);
 }
 
-// (sin, cos)(a + d) from (sin, cos)(a): series to d^7 / d^6 when
-// |d| < 2^-6 (truncation < 1e-19, below fp64 resolution of the result),
-// otherwise a direct sincos of the new angle `x`.
-__device__ __forceinline__ void rotate64(double s, double c, double d, double x, double& so,
-                                         double& co) {
-  if (fabs(d) < 0.0009765625) {
-    // |d| < 2^-10: sin d = d - d^3/6, cos d = 1 - d^2/2 + d^4/24 (truncation
-    // d^5/120 < 8e-18, below fp64 resolution of the result)
+// |x| < 2^-k as an integer test of the high word (ALU pipe, not FP64)
+__device__ __forceinline__ bool small_abs(double x, unsigned hi_bound) {
+  return ((unsigned)__double2hiint(x) & 0x7fffffffu) < hi_bound;
+}
+constexpr unsigned kHi2m6 = 0x3F900000u;     // 2^-6
+constexpr unsigned kHi2m8 = 0x3F700000u;     // 2^-8
+constexpr unsigned kHi2m10 = 0x3F500000u;    // 2^-10
+
+// sin/cos providers.  TrigTab is the propagate kernels' evaluation: a
+// 512-entry (sin, cos)(2 pi i / 512) table in shared memory and a short
+// polynomial on the remainder |r| <= pi/512 (sin to r^5, truncation r^7/5040
+// < 1e-19; cos to r^4, truncation r^6/720 < 1e-16), 14 fp64 operations and
+// one 16-byte shared load.  The reduction is two-part Cody-Waite (C1 has 27
+// significant bits, so k C1 is exact for |k| < 2^26, |x| < 8e5 rad), and the
+// quotient k comes from the 1.5 2^52 shifter, whose low word is the table
+// index.  TrigLib (libdevice) serves the init kernel.
+constexpr int kTabN = 512;
+constexpr double kTabScale = 81.487330863050417;       // 512 / (2 pi)
+constexpr double kTabC1 = 0.012271846295334399;         // 2 pi / 512 to 27 bits
+constexpr double kTabC2 = 7.750731091254222e-12;         // 2 pi / 512 - C1
+constexpr double kShift52 = 6755399441055744.0;         // 1.5 * 2^52
+// fp64 constants whose low words are nonzero live in constant memory, so
+// DFMA reads them as c[][] operands instead of rematerialising 64-bit
+// immediates into register pairs every cell
+__constant__ double c_k64[6] = {kTabScale, kTabC1, kTabC2, 1.0 / 120.0, -1.0 / 6.0, 1.0 / 24.0};
+#define K_TABSCALE c_k64[0]
+#define K_TABC1 c_k64[1]
+#define K_TABC2 c_k64[2]
+#define K_1_120 c_k64[3]
+#define K_M1_6 c_k64[4]
+#define K_1_24 c_k64[5]
+
+struct TrigTab {
+  const double2* tab;
+  __device__ __forceinline__ void operator()(double x, double& s, double& c) const {
+    const double y = fma(x, K_TABSCALE, kShift52);
+    const double k = y - kShift52;
+    const int idx = __double2loint(y) & (kTabN - 1);
+    double r = fma(-k, K_TABC1, x);
+    r = fma(-k, K_TABC2, r);
+    const double z = r * r;
+    const double sr = fma(r * z, fma(z, K_1_120, K_M1_6), r);
+    const double cr = fma(z, fma(z, K_1_24, -0.5), 1.0);
+    const double2 e = tab[idx];                          // (sin a, cos a)
+    s = fma(e.x, cr, e.y * sr);
+    c = fma(e.y, cr, -e.x * sr);
+  }
+  // the same with the sine series one term shorter (r^5/120 < 8e-14): for
+  // angles that reach the state scaled down (argpm by em, xmdf by drag)
+  __device__ __forceinline__ void short_sin(double x, double& s, double& c) const {
+    const double y = fma(x, K_TABSCALE, kShift52);
+    const double k = y - kShift52;
+    const int idx = __double2loint(y) & (kTabN - 1);
+    double r = fma(-k, K_TABC1, x);
+    r = fma(-k, K_TABC2, r);
+    const double z = r * r;
+    const double sr = fma(r * z, K_M1_6, r);
+    const double cr = fma(z, fma(z, K_1_24, -0.5), 1.0);
+    const double2 e = tab[idx];
+    s = fma(e.x, cr, e.y * sr);
+    c = fma(e.y, cr, -e.x * sr);
+  }
+};
+// table-free alternative (SGP4B_F64_TABLE=0): quadrant reduction and
+// degree-13/14 polynomials, coefficients in constant memory
+__constant__ double c_sin_poly[6] = {
+    -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+    2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10};
+__constant__ double c_cos_poly[6] = {
+    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11};
+__constant__ double c_pio2[4] = {1.57079632673412561417e+00, 6.07710050630396597660e-11,
+                                 2.02226624879595063154e-21, 6.36619772367581382433e-01};
+struct TrigPoly {
+  const double2* tab;                                    // unused
+  __device__ __forceinline__ void operator()(double x, double& s, double& c) const {
+    const double y = fma(x, c_pio2[3], kShift52);
+    const double k = y - kShift52;
+    const int q = __double2loint(y) & 3;
+    double r = fma(-k, c_pio2[0], x);
+    r = fma(-k, c_pio2[1], r);
+    r = fma(-k, c_pio2[2], r);
+    const double z = r * r;
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, c_sin_poly[5], c_sin_poly[4]),
+                                                   c_sin_poly[3]), c_sin_poly[2]), c_sin_poly[1]),
+                          c_sin_poly[0]);
+    const double sr = fma(r * z, ps, r);
+    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, c_cos_poly[5], c_cos_poly[4]),
+                                                   c_cos_poly[3]), c_cos_poly[2]), c_cos_poly[1]),
+                          c_cos_poly[0]);
+    const double cr = fma(z * z, pc, fma(-0.5, z, 1.0));
+    const double s0 = (q & 1) ? cr : sr;
+    const double c0 = (q & 1) ? sr : cr;
+    s = (q & 2) ? -s0 : s0;
+    c = ((q + 1) & 2) ? -c0 : c0;
+  }
+  __device__ __forceinline__ void short_sin(double x, double& s, double& c) const { (*this)(x, s, c); }
+};
+#ifndef SGP4B_F64_TABLE
+#define SGP4B_F64_TABLE 1
+#endif
+struct TrigLib {
+  __device__ __forceinline__ void operator()(double x, double& s, double& c) const { sincos(x, &s, &c); }
+  __device__ __forceinline__ void short_sin(double x, double& s, double& c) const { sincos(x, &s, &c); }
+};
+
+// (sin, cos)(a + d) from (sin, cos)(a): series to d^5 / d^4 for |d| < 2^-8
+// (truncation d^7/5040 < 1e-20, d^6/720 < 5e-18), otherwise a direct
+// evaluation of the new angle x.
+template <class Trig>
+__device__ __forceinline__ void rotate64(double s, double c, double d, double x, const Trig& tr,
+                                         double& so, double& co) {
+  if (small_abs(d, kHi2m8)) {
     const double d2 = d * d;
-    const double sd = fma(d * d2, -1.0 / 6.0, d);
-    const double cd = fma(d2, fma(d2, 1.0 / 24.0, -0.5), 1.0);
-    so = fma(s, cd, c * sd);
-    co = fma(c, cd, -s * sd);
-  } else if (fabs(d) < 0.015625) {
-    const double d2 = d * d;
-    const double sd = d * fma(d2, fma(d2, fma(d2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
-    const double cd = fma(d2, fma(d2, fma(d2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+    const double sd = fma(d * d2, fma(d2, K_1_120, K_M1_6), d);
+    const double cd = fma(d2, fma(d2, K_1_24, -0.5), 1.0);
     so = fma(s, cd, c * sd);
     co = fma(c, cd, -s * sd);
   } else {
-    sincos64(x, &so, &co);
+    tr(x, so, co);
   }
 }
 
-// fp64 cell (kernel.py:352-510), the parity variant: fp64 throughout, with
-// the reference's guards, thresholds and code precedence.  It departs from
-// the reference's operation order only where the result is unchanged to far
-// below the 1 mm / 1e-6 km/s budget (measured ~1e-9 km):
-//   * angles are never floor-reduced: every angle only reaches sin/cos (whose
-//     Cody-Waite reduction is exact), and the Kepler argument is formed as
-//     u = (mo + argpo) + (mdot + argpdot) t + no templ + xlcof axnl / pl_lp
-//     (mm + argpm; the drag terms cancel) with E carried as u + d;
-//   * sqrt(am) = sqrt(am0) |tempa| and nm = no / |tempa|^3 (the pow of
-//     kernel.py:397-401 with am0 = (xke/no)^(2/3) hoisted);
-//   * sin/cos are evaluated once per angle family: the drag correction of
-//     the mean anomaly, the Newton updates of E and the J2 short-period
-//     corrections of su and xinc are rotations (rotate64); the atan2 of
-//     kernel.py:455 is replaced by normalising (sin u, cos u);
-//   * sqrt(pl) = sqrt(am) betal, and reciprocals use two Newton steps.
-template <class RT>
-__device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cell64& o) {
+// orientation and output (kernel.py:472-493) from (sin, cos) su, xnode, xinc
+__device__ __forceinline__ void orient64(double mr, double mv, double rv, double sinsu,
+                                         double cossu, double snod, double cnod, double sini,
+                                         double cosi, Cell64& o) {
+  const double xmx = -snod * cosi;
+  const double xmy = cnod * cosi;
+  const double ra = mr * sinsu, rb = mr * cossu;
+  o.r[0] = fma(xmx, ra, cnod * rb);
+  o.r[1] = fma(xmy, ra, snod * rb);
+  o.r[2] = sini * ra;
+  const double va = fma(mv, sinsu, rv * cossu);
+  const double vb = fma(mv, cossu, -rv * sinsu);
+  o.v[0] = fma(xmx, va, cnod * vb);
+  o.v[1] = fma(xmy, va, snod * vb);
+  o.v[2] = sini * va;
+}
+
+// General fp64 cell: every orbit class, the reference's guards, thresholds
+// and code precedence, and the reference's Kepler loop (<= 10 Newton steps,
+// +-0.95 clamp, 1e-12 freeze).  It departs from the reference operation
+// order only where results move far below the 1 mm / 1e-6 km/s budget
+// (measured ~1e-9 km): per-satellite products folded into the record (fp64),
+// no floor-mods (every angle only reaches sin/cos, whose reduction is exact),
+// the Kepler argument formed as u = (mo + argpo) + (mdot + argpdot) t +
+// no templ + xlcof axnl / pl_lp (mm + argpm: the drag terms cancel) with E
+// carried as u + d, sin/cos carried through the small drag, Newton and J2
+// corrections by rotation (rotate64), and the atan2 of kernel.py:455
+// replaced by normalising (sin u, cos u).
+template <class RT, class Trig>
+__device__ __forceinline__ void cell64_general(const RT& R, double t, double re, double vkm,
+                                               const Trig& tr, Cell64& o) {
   const double tiny = DBL_MIN;
-  const double j2 = g.j2, re = g.re;
   const int flags = R.flags();
   const bool isimp = flags & FLAG_ISIMP;
 
   // secular gravity and atmospheric drag  kernel.py:365-391
-  const double argpdf = fma(R[S_ARGPDOT], t, R[S_ARGPO]);
+  const double argpdf = fma(R[Q_ARGPDOT], t, R[Q_ARGPO]);
   const double t2 = t * t;
-  const double nodem = fma(R[S_NODECF], t2, fma(R[S_NODEDOT], t, R[S_NODEO]));
-  double tempa = fma(-R[S_CC1], t, 1.0);
-  double tempe = R[S_BC4] * t;
-  double templ = R[S_T2COF] * t2;
-  double argpm = argpdf;
-  if (!isimp) {
-    const double xmdf = fma(R[S_MDOT], t, R[S_MO]);
+  const double nodem = fma(R[Q_NODECF], t2, fma(R[Q_NODEDOT], t, R[Q_NODEO]));
+  const double usec = fma(R[Q_UDOT], t, R[Q_U0]);
+  double sqam, nol, argpm, em;
+  if (isimp) {
+    sqam = fma(R[Q_SC1], t, R[Q_S]);
+    nol = R[Q_N2] * t2;
+    em = fma(-R[Q_BC4], t, R[Q_E0]);
+    argpm = argpdf;
+  } else {
+    const double xmdf = fma(R[Q_MDOT], t, R[Q_MO]);
     double sx, cx;
-    sincos64(xmdf, &sx, &cx);
-    const double delmtemp = fma(R[S_ETA], cx, 1.0);
-    const double delm = R[S_XMCOF] * fma(delmtemp * delmtemp, delmtemp, -R[S_DELMO]);
-    const double temp = fma(R[S_OMGCOF], t, delm);
+    tr(xmdf, sx, cx);
+    const double temp = fma(fma(fma(cx, R[Q_A3], R[Q_A2]), cx, R[Q_A1]), cx,
+                            fma(R[Q_OMGCOF], t, R[Q_A0]));
     argpm = argpdf - temp;
-    tempa = fma(-t2, fma(t, fma(t, R[S_D4], R[S_D3]), R[S_D2]), tempa);
+    sqam = fma(t, fma(t, fma(t, fma(t, R[Q_SD4], R[Q_SD3]), R[Q_SD2]), R[Q_SC1]), R[Q_S]);
+    nol = t2 * fma(t, fma(t, fma(t, R[Q_N5], R[Q_N4]), R[Q_N3]), R[Q_N2]);
     double smm, cmm;
-    rotate64(sx, cx, temp, xmdf + temp, smm, cmm);       // sin(mm)
-    tempe = fma(R[S_BC5], smm - R[S_SINMAO], tempe);
-    templ = fma(t2 * t, fma(t, fma(t, R[S_T5COF], R[S_T4COF]), R[S_T3COF]), templ);
+    rotate64(sx, cx, temp, xmdf + temp, tr, smm, cmm);    // sin(mm)
+    em = fma(-R[Q_BC5], smm, fma(-R[Q_BC4], t, R[Q_E0]));
   }
 
   // mean motion / eccentricity update  kernel.py:393-414
-  const double atempa = fabs(tempa);
-  const double am = gmax(R[S_AM0] * tempa * tempa, tiny);       // am_safe
-  const double sqam = R[S64_SQAM0] * atempa;                    // sqrt(am)
-  const double ita = rcp64(atempa);
-  const double nm = R[S64_NOSAFE] * (ita * ita * ita);          // xke / am^1.5
-  double em = R[S_ECCO] - tempe;
+  const double asq = fabs(sqam);                            // sqrt(am)
+  const double am = gmax(sqam * sqam, tiny);                // am_safe
+  const double irs = rcp64(asq);
+  const double nmx = irs * irs * irs;                       // nm / xke = am^-1.5
   const bool bad_em = (em >= 1.0) || (em < -0.001);
   em = em < 1.0e-6 ? 1.0e-6 : em;
 
   // long-period periodics  kernel.py:419-431
   double sa, ca;
-  sincos64(argpm, &sa, &ca);
+  tr(argpm, sa, ca);
   const double axnl = em * ca;
   const double ilp = rcp64(gmax(am * fma(-em, em, 1.0), tiny));
-  const double aynl = fma(em, sa, ilp * R[S_AYCOF]);
-  const double u = fma(ilp * R[S_XLCOF], axnl,
-                       fma(R[S_NO], templ, fma(R[S_UDOT], t, R[S_U0])));
+  const double aynl = fma(em, sa, ilp * R[Q_AYCOF]);
+  const double u = fma(ilp * R[Q_XLCOF], axnl, usec + nol);
 
   // Kepler  kernel.py:325-349: E = u + d, (sin, cos) E carried along the
   // Newton updates by rotation, the reference's clamp and 1e-12 freeze
   double sineo1, coseo1, d = 0.0;
-  sincos64(u, &sineo1, &coseo1);
-  // Newton from E0 = u: |E - E_k| <~ (e/2)^(2^k - 1) e^(2^k), so for the
-  // fp32 classes e < 0.004 and e < 0.1 (flags) two and three steps land
-  // below 1e-17 rad, where the reference's extra step only confirms the
-  // 1e-12 freeze; other orbits run the reference loop
-  const int kfix = (flags >> KEPLER_SHIFT) & 0xf;
-  const int kmax = kfix == 1 ? 2 : kfix == 2 ? 3 : 10;
+  tr(u, sineo1, coseo1);
   bool active = true;
 #pragma unroll 1
-  for (int it = 0; it < kmax && active; ++it) {
+  for (int it = 0; it < 10 && active; ++it) {
     const double den = fma(-sineo1, aynl, fma(-coseo1, axnl, 1.0));
     const double num = fma(axnl, sineo1, fma(-aynl, coseo1, -d));
     double tem5 = num * rcp64(den);
     tem5 = tem5 >= 0.95 ? 0.95 : (tem5 <= -0.95 ? -0.95 : tem5);
     d += tem5;
-    rotate64(sineo1, coseo1, tem5, u + d, sineo1, coseo1);
+    rotate64(sineo1, coseo1, tem5, u + d, tr, sineo1, coseo1);
     active = fabs(tem5) >= 1.0e-12;
   }
 
@@ -482,61 +564,226 @@ __device__ __forceinline__ void cell64(const RT& R, double t, const Grav& g, Cel
   const double rl = am * (1.0 - ecose);
   const double irl = rcp64(rl == 0.0 ? tiny : rl);
   const double betal = sqrt64(gmax(omel2, tiny));
-  const double rdotl = sqam * esine * irl;
+  const double rdv = (asq * vkm) * esine * irl;
   // sqrt(pl_safe) = sqrt(am) betal whenever pl >= tiny
-  const double rvdotl = (pl >= tiny ? sqam * betal : sqrt64(pl_safe)) * irl;
+  const double rvdv = (pl >= tiny ? asq * betal : sqrt64(pl_safe)) * (irl * vkm);
   const double tq = esine * rcp64(1.0 + betal);
   // (sin u, cos u) normalised: the reference's am/rl factor is positive and
-  // only the direction reaches sin/cos(su)
+  // only the direction reaches su
   const double sn = fma(-axnl, tq, sineo1 - aynl);
   const double cs = fma(aynl, tq, coseo1 - axnl);
   const double inrm = rsqrt64(fma(sn, sn, cs * cs));
   const double sinu = sn * inrm, cosu = cs * inrm;
-  const double sin2u = (cosu + cosu) * sinu;
-  const double cos2u = fma(-2.0 * sinu, sinu, 1.0);
+  const double s2u = sinu + sinu;
+  const double sin2u = s2u * cosu;
+  const double cos2u = fma(-s2u, sinu, 1.0);
   const double ipl = rcp64(pl_safe);
-  const double temp1 = 0.5 * j2 * ipl;
-  const double temp2 = temp1 * ipl;
+  const double ipl2 = ipl * ipl;
 
-  // short-period periodics  kernel.py:463-469
-  const double con41 = R[S_CON41], x1mth2 = R[S_X1MTH2];
-  const double sinip = R[S_SINIO], cosip = R[S_COSIO];
-  const double mrt = fma(rl, fma(-1.5 * temp2 * betal, con41, 1.0), 0.5 * temp1 * x1mth2 * cos2u);
-  const double dsu = -0.25 * temp2 * R[S_X7THM1] * sin2u;
-  const double xnode = fma(1.5 * temp2 * cosip, sin2u, nodem);
-  const double dinc = 1.5 * temp2 * cosip * sinip * cos2u;
-  const double nmx = nm * temp1 * g.inv_xke;
-  const double mvt = fma(-nmx * x1mth2, sin2u, rdotl);
-  const double rvdot = fma(nmx, fma(x1mth2, cos2u, 1.5 * con41), rvdotl);
+  // short-period periodics  kernel.py:463-469 (0.5 j2, re, vkm folded)
+  const double mrt = fma(rl, fma(ipl2 * R[Q_K41R], betal, re), (ipl * R[Q_KXR]) * cos2u);
+  const double t2s = ipl2 * sin2u;
+  const double dsu = t2s * R[Q_QX];
+  const double xnode = fma(t2s, R[Q_C15CO], nodem);
+  const double dinc = (ipl2 * cos2u) * R[Q_C15CS];
+  const double nmt = nmx * ipl;
+  const double mv = fma(-(nmt * R[Q_X1V]), sin2u, rdv);
+  const double rv = fma(nmt, fma(cos2u, R[Q_X1V], R[Q_C41V]), rvdv);
 
   // orientation  kernel.py:472-493
   double sinsu, cossu, snod, cnod, sini, cosi;
-  if (fabs(dsu) < 0.015625)
-    rotate64(sinu, cosu, dsu, 0.0, sinsu, cossu);
+  if (small_abs(dsu, kHi2m8))
+    rotate64(sinu, cosu, dsu, 0.0, tr, sinsu, cossu);
   else
-    sincos64(atan2(sinu, cosu) + dsu, &sinsu, &cossu);
-  sincos64(xnode, &snod, &cnod);
-  rotate64(sinip, cosip, dinc, R[S_INCLO] + dinc, sini, cosi);
-  const double xmx = -snod * cosi;
-  const double xmy = cnod * cosi;
-  const double mr = mrt * re;
-  const double ra = mr * sinsu, rb = mr * cossu;
-  o.r[0] = fma(xmx, ra, cnod * rb);
-  o.r[1] = fma(xmy, ra, snod * rb);
-  o.r[2] = sini * ra;
-  const double mv = mvt * g.vkm, rv = rvdot * g.vkm;
-  const double va = fma(mv, sinsu, rv * cossu);
-  const double vb = fma(mv, cossu, -rv * sinsu);
-  o.v[0] = fma(xmx, va, cnod * vb);
-  o.v[1] = fma(xmy, va, snod * vb);
-  o.v[2] = sini * va;
+    tr(atan2(sinu, cosu) + dsu, sinsu, cossu);
+  tr(xnode, snod, cnod);
+  rotate64(R[Q_SINIO], R[Q_COSIO], dinc, R[Q_INCLO] + dinc, tr, sini, cosi);
+  orient64(mrt, mv, rv, sinsu, cossu, snod, cnod, sini, cosi, o);
 
   // _first_error + init merge  kernel.py:495-502, 529-534 (bad_nm is folded
-  // into the persistent code field of the record)
-  const bool decayed = mrt < 1.0;
-  const int code = bad_em ? 1 : bad_pl ? 4 : decayed ? 6 : 0;
-  const int persistent = (flags >> CODE_SHIFT) & 0xff;
+  // into the persistent code field of the record); decayed: mrt < 1 earth
+  // radius, i.e. mr < re
+  const int code = bad_em ? 1 : bad_pl ? 4 : (mrt < re) ? 6 : 0;
+  const int persistent = (flags >> CODE_SHIFT) & 0x7fffff;
   o.code = persistent != 0 ? persistent : code;
+}
+
+// the general cell as one out-of-line copy, storing its own outputs: the
+// fallback of the fast cell (nothing of the fast path's state escapes to
+// local memory)
+using TrigGrid = std::conditional<SGP4B_F64_TABLE != 0, TrigTab, TrigPoly>::type;
+
+__device__ __noinline__ void cell64_fallback(const double* rec, double t, double re, double vkm,
+                                             const double2* tab, double* out, int64_t ps,
+                                             int32_t* cout) {
+  RecS<double> R;
+  R.p = rec;
+  Cell64 o;
+  cell64_general(R, t, re, vkm, TrigGrid{tab}, o);
+  st_cs(out, o.r[0]);
+  st_cs(out + ps, o.r[1]);
+  st_cs(out + 2 * ps, o.r[2]);
+  st_cs(out + 3 * ps, o.v[0]);
+  st_cs(out + 4 * ps, o.v[1]);
+  st_cs(out + 5 * ps, o.v[2]);
+  st_cs(cout, o.code);
+}
+
+// 64-bit integer views of doubles: ordering tests on the ALU pipe (the FP64
+// pipe is the binding resource of the fp64 cell).  Valid for finite x.
+__device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
+// x < b for a constant b > 0: negative doubles are negative int64s
+__device__ __forceinline__ bool lt_pos(double x, long long bbits) { return dbits(x) < bbits; }
+// x < b for a constant b < 0: among doubles with the sign bit set, the
+// unsigned bit pattern grows with the magnitude; positives are below them all
+__device__ __forceinline__ bool lt_neg(double x, unsigned long long bbits) {
+  return (unsigned long long)dbits(x) > bbits;
+}
+constexpr long long kBits1em6 = 0x3EB0C6F7A0B5ED8DLL;          // 1.0e-6
+constexpr unsigned long long kBitsM1em3 = 0xBF50624DD2F1A9FCULL; // -0.001
+constexpr unsigned kHi4em3 = 0x3F70624Du;                        // hi word of 0.004
+constexpr unsigned kHiTiny = 0x20C00000u;                        // ~6e-151
+
+// Fast fp64 cell for near-circular orbits (|em| < 0.004 at this cell, every
+// Starlink-like satellite): with el = |(axnl, aynl)| < 0.0052, el2 < 3e-5,
+//   * two Newton steps reach the fixed point of the reference's loop (error
+//     el^7/8 < 1e-17; the first step's 1/den as 1 + q + q^2, the second's as
+//     1 + q + q^2 + q^3, |q| < el: the second step absorbs the first
+//     truncation and leaves q^4 of a 1e-7 step; its rotation has cos = 1 to
+//     2.5e-15);
+//   * betal = 1 - el2/2 - el2^2/8, 1/pl = (1 + el2 + el2^2)/am,
+//     1/pl_lp = (1 + em^2 + em^4)/am, 1/(1 + betal) = 1/2 + el2/8 + el2^2/16
+//     (truncations < 3e-14 relative, on terms of order 1e-3), pl > 0 so the
+//     SEMILATUS code cannot occur;
+//   * (sin u, cos u) = (am/rl) (...) as the reference forms them (unit norm
+//     at the converged E);
+//   * sin(mm) = sin(xmdf + temp) to temp^3 (|temp| < 2^-6; it only enters
+//     through bstar cc5 < 4e-6), the J2 rotations of su and xinc as series
+//     (|dsu|, |dinc| < 2^-10; near-Earth orbits have |dsu| < 8.1e-4 and
+//     |dinc| < 4.1e-4), and the first Newton rotation to d^3 and d^4;
+//   * sin/cos of argpm (scaled by em < 0.004) and of xmdf (through the drag
+//     coefficients) with the sine series one term shorter (r^5/120 < 8e-14).
+// The cell is straight-line code; a cell outside that domain (|em| >= 0.004,
+// a NaN, sqrt(am) < 6e-151, or a larger drag / J2 angle) reports false and
+// the caller runs the general cell instead.  The test is per cell, so a
+// cell's value never depends on which other cells share its launch
+// (batch == scalar).
+template <bool ISIMP, class RT, class Trig>
+__device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long long re_bits,
+                                          double vkm, const Trig& tr, Cell64& o) {
+  const int flags = R.flags();
+  const double argpdf = fma(R[Q_ARGPDOT], t, R[Q_ARGPO]);
+  const double t2 = t * t;
+  const double nodem = fma(R[Q_NODECF], t2, fma(R[Q_NODEDOT], t, R[Q_NODEO]));
+  const double usec = fma(R[Q_UDOT], t, R[Q_U0]);
+  double sqam, nol, argpm, em;
+  bool ok = true;
+  if constexpr (ISIMP) {
+    sqam = fma(R[Q_SC1], t, R[Q_S]);
+    nol = R[Q_N2] * t2;
+    em = fma(-R[Q_BC4], t, R[Q_E0]);
+    argpm = argpdf;
+  } else {
+    const double xmdf = fma(R[Q_MDOT], t, R[Q_MO]);
+    double sx, cx;
+    tr.short_sin(xmdf, sx, cx);
+    const double temp = fma(fma(fma(cx, R[Q_A3], R[Q_A2]), cx, R[Q_A1]), cx,
+                            fma(R[Q_OMGCOF], t, R[Q_A0]));
+    argpm = argpdf - temp;
+    sqam = fma(t, fma(t, fma(t, fma(t, R[Q_SD4], R[Q_SD3]), R[Q_SD2]), R[Q_SC1]), R[Q_S]);
+    nol = t2 * fma(t, fma(t, fma(t, R[Q_N5], R[Q_N4]), R[Q_N3]), R[Q_N2]);
+    const double tt = temp * temp;
+    const double smm = fma(sx, fma(tt, -0.5, 1.0), (cx * temp) * fma(tt, K_M1_6, 1.0));
+    em = fma(-R[Q_BC5], smm, fma(-R[Q_BC4], t, R[Q_E0]));
+    ok = small_abs(temp, kHi2m6);
+  }
+  const double asq = __longlong_as_double(dbits(sqam) & 0x7fffffffffffffffLL);   // |sqam|
+  ok = ok && small_abs(em, kHi4em3) &&
+       ((unsigned)__double2hiint(asq) & 0x7fffffffu) >= kHiTiny;
+  const bool bad_em = lt_neg(em, kBitsM1em3);
+  em = lt_pos(em, kBits1em6) ? 1.0e-6 : em;
+
+  // mean motion  kernel.py:397-401 (nm / xke = am^-1.5)
+  const double am = sqam * sqam;
+  const double irs = rcp64(asq);
+  const double inv_am = irs * irs;
+  const double nmx = inv_am * irs;
+
+  // long-period periodics  kernel.py:419-431
+  double sa, ca;
+  tr.short_sin(argpm, sa, ca);
+  const double axnl = em * ca;
+  const double em2 = em * em;
+  const double ilp = fma(inv_am, fma(em2, em2, em2), inv_am);
+  const double aynl = fma(em, sa, ilp * R[Q_AYCOF]);
+  const double u = fma(ilp * R[Q_XLCOF], axnl, usec + nol);
+
+  // Kepler  kernel.py:325-349, two Newton steps from E0 = u
+  double s0, c0;
+  tr(u, s0, c0);
+  double q = fma(c0, axnl, s0 * aynl);
+  double num = fma(axnl, s0, -aynl * c0);
+  const double d1 = fma(num, fma(q, q, q), num);
+  const double dd = d1 * d1;
+  const double sd = fma(d1 * dd, K_M1_6, d1);         // d^5/120 < 4e-14
+  const double cd = fma(dd, fma(dd, K_1_24, -0.5), 1.0);
+  const double s1 = fma(s0, cd, c0 * sd), c1 = fma(c0, cd, -s0 * sd);
+  q = fma(c1, axnl, s1 * aynl);
+  num = fma(axnl, s1, fma(-aynl, c1, -d1));
+  const double d2 = fma(num, q, num) * fma(q, q, 1.0);
+  const double sineo1 = fma(c1, d2, s1), coseo1 = fma(-s1, d2, c1);
+
+  // short-period preliminaries  kernel.py:440-460
+  const double ecose = fma(axnl, coseo1, aynl * sineo1);
+  const double esine = fma(axnl, sineo1, -aynl * coseo1);
+  const double el2 = fma(axnl, axnl, aynl * aynl);
+  const double ome = 1.0 - ecose;
+  const double iome = rcp64(ome);                                 // am / rl
+  const double rl = am * ome;
+  const double betal = fma(el2, fma(el2, -0.125, -0.5), 1.0);
+  const double ipl = fma(inv_am, fma(el2, el2, el2), inv_am);
+  const double tq = esine * fma(el2, fma(el2, 0.0625, 0.125), 0.5);
+  const double sqvk = (irs * vkm) * iome;                         // sqrt(am)/rl km/s
+  const double rdv = sqvk * esine;
+  const double rvdv = sqvk * betal;
+  const double sinu = fma(-axnl, tq, sineo1 - aynl) * iome;
+  const double cosu = fma(aynl, tq, coseo1 - axnl) * iome;
+  const double s2u = sinu + sinu;
+  const double sin2u = s2u * cosu;
+  const double cos2u = fma(-s2u, sinu, 1.0);
+  const double ipl2 = ipl * ipl;
+
+  // short-period periodics  kernel.py:463-469
+  const double mr = fma(rl, fma(ipl2 * R[Q_K41R], betal, re), (ipl * R[Q_KXR]) * cos2u);
+  const double t2s = ipl2 * sin2u;
+  const double dsu = t2s * R[Q_QX];
+  const double xnode = fma(t2s, R[Q_C15CO], nodem);
+  const double dinc = (ipl2 * cos2u) * R[Q_C15CS];
+  const double nmt = nmx * ipl;
+  const double mv = fma(-(nmt * R[Q_X1V]), sin2u, rdv);
+  const double rv = fma(nmt, fma(cos2u, R[Q_X1V], R[Q_C41V]), rvdv);
+  ok = ok && small_abs(dsu, kHi2m10) && small_abs(dinc, kHi2m10);
+
+  // orientation  kernel.py:472-493: su = u + dsu, xinc = inclo + dinc by
+  // rotation, |d| < 2^-10: sin d = d - d^3/6, cos d = 1 - d^2/2 (truncation
+  // < 4e-14)
+  const double du2 = dsu * dsu;
+  const double sdu = fma(dsu * du2, K_M1_6, dsu);
+  const double cdu = fma(du2, -0.5, 1.0);
+  const double sinsu = fma(sinu, cdu, cosu * sdu), cossu = fma(cosu, cdu, -sinu * sdu);
+  double snod, cnod;
+  tr(xnode, snod, cnod);
+  const double di2 = dinc * dinc;
+  const double sdi = fma(dinc * di2, K_M1_6, dinc);
+  const double cdi = fma(di2, -0.5, 1.0);
+  const double sini = fma(R[Q_SINIO], cdi, R[Q_COSIO] * sdi);
+  const double cosi = fma(R[Q_COSIO], cdi, -R[Q_SINIO] * sdi);
+  orient64(mr, mv, rv, sinsu, cossu, snod, cnod, sini, cosi, o);
+
+  const int code = bad_em ? 1 : lt_pos(mr, re_bits) ? 6 : 0;
+  const int persistent = (flags >> CODE_SHIFT) & 0x7fffff;
+  o.code = persistent != 0 ? persistent : code;
+  return ok;
 }
 
 // ======================================================================
@@ -921,7 +1168,7 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
 
   // _first_error 2 > 1 > 4 > 6 and the init merge  kernel.py:497-502, 529-534
   // (decayed: mrt < 1 earth radius, i.e. mr < re)
-  const int persistent = (flags >> CODE_SHIFT) & 0xff;     // includes bad_nm -> 2
+  const int persistent = (flags >> CODE_SHIFT) & 0x7fffff; // includes bad_nm -> 2
 #pragma unroll
   for (int h = 0; h < NC; ++h) {
     const int cellc = bad_em[h] ? 1 : bad_pl[h] ? 4 : (comp(mr, h) < g.re_f) ? 6 : 0;
@@ -968,7 +1215,7 @@ __device__ __forceinline__ int record_flags(const double* f, int init_code, bool
   int persistent = init_code == 6 ? 0 : init_code;
   if (persistent == 0 && bad_nm) persistent = 2;
   return (isimp ? FLAG_ISIMP : 0) | (bad_nm ? FLAG_BAD_NM : 0) |
-         (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0xff) << CODE_SHIFT);
+         (kepler_iters_for(f[F_ECCO]) << KEPLER_SHIFT) | ((persistent & 0x7fffff) << CODE_SHIFT);
 }
 
 // fp64 record values (flags slot left 0; see record_flags)
@@ -1024,9 +1271,56 @@ template <>
 __device__ __forceinline__ void store_record<double>(const double* f, const double* v, int flags,
                                                      bool isimp, const Grav& g,
                                                      double* __restrict__ rec) {
+  double o[S_COUNT];
 #pragma unroll
-  for (int i = 0; i < S_COUNT; ++i) rec[i] = v[i];
-  rec[S_FLAGS] = __longlong_as_double((long long)flags);
+  for (int i = 0; i < S_COUNT; ++i) o[i] = 0.0;
+  const double hj2 = 0.5 * g.j2, bstar = f[F_BSTAR], no = v[S_NO];
+  const double s = v[S64_SQAM0];
+  o[Q_ARGPO] = f[F_ARGPO];
+  o[Q_ARGPDOT] = f[F_ARGPDOT];
+  o[Q_NODEO] = f[F_NODEO];
+  o[Q_NODEDOT] = f[F_NODEDOT];
+  o[Q_NODECF] = f[F_NODECF];
+  o[Q_MO] = f[F_MO];
+  o[Q_MDOT] = f[F_MDOT];
+  o[Q_U0] = v[S_U0];
+  o[Q_UDOT] = v[S_UDOT];
+  o[Q_S] = s;
+  o[Q_SC1] = -s * f[F_CC1];
+  o[Q_N2] = no * f[F_T2COF];
+  o[Q_E0] = f[F_ECCO];
+  o[Q_BC4] = bstar * f[F_CC4];
+  if (!isimp) {                       // kernel.py:371-391 (zero in isimp records)
+    const double eta = f[F_ETA], xmcof = f[F_XMCOF];
+    o[Q_A0] = xmcof * (1.0 - f[F_DELMO]);
+    o[Q_A1] = 3.0 * xmcof * eta;
+    o[Q_A2] = 3.0 * xmcof * eta * eta;
+    o[Q_A3] = xmcof * eta * eta * eta;
+    o[Q_OMGCOF] = f[F_OMGCOF];
+    o[Q_SD2] = -s * f[F_D2];
+    o[Q_SD3] = -s * f[F_D3];
+    o[Q_SD4] = -s * f[F_D4];
+    o[Q_N3] = no * f[F_T3COF];
+    o[Q_N4] = no * f[F_T4COF];
+    o[Q_N5] = no * f[F_T5COF];
+    o[Q_BC5] = bstar * f[F_CC5];
+    o[Q_E0] = f[F_ECCO] + bstar * f[F_CC5] * f[F_SINMAO];
+  }
+  o[Q_AYCOF] = f[F_AYCOF];
+  o[Q_XLCOF] = f[F_XLCOF];
+  o[Q_K41R] = -1.5 * f[F_CON41] * hj2 * g.re;
+  o[Q_KXR] = 0.5 * f[F_X1MTH2] * hj2 * g.re;
+  o[Q_QX] = -0.25 * f[F_X7THM1] * hj2;
+  o[Q_C15CO] = 1.5 * v[S_COSIO] * hj2;
+  o[Q_C15CS] = 1.5 * v[S_COSIO] * v[S_SINIO] * hj2;
+  o[Q_X1V] = f[F_X1MTH2] * hj2 * g.vkm;
+  o[Q_C41V] = 1.5 * f[F_CON41] * hj2 * g.vkm;
+  o[Q_SINIO] = v[S_SINIO];
+  o[Q_COSIO] = v[S_COSIO];
+  o[Q_INCLO] = f[F_INCLO];
+  o[Q_FLAGS] = __longlong_as_double((long long)flags);
+#pragma unroll
+  for (int i = 0; i < S_COUNT; ++i) rec[i] = o[i];
 }
 
 // reduce an angle to [-pi, pi): fp32 has the most resolution there
@@ -1223,14 +1517,15 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   code = bad_n ? 2 : bad_e ? 1 : deep_space ? 7 : 0;
   isimp_out = isimp;
 
-  // epoch evaluation  :316-322
-  Rec<double> R;
-  record_values(f, g, R.v);
-#pragma unroll
-  for (int i = 0; i < S_COUNT; ++i) v[i] = R.v[i];
-  R.v[S_FLAGS] = __longlong_as_double((long long)record_flags(f, 0, isimp));
+  // epoch evaluation  :316-322 (the general cell on an fp64 record built
+  // with no persistent code)
+  record_values(f, g, v);
+  double rec[S_COUNT];
+  store_record<double>(f, v, record_flags(f, 0, isimp), isimp, g, rec);
+  RecS<double> R;
+  R.p = rec;
   Cell64 c0;
-  cell64(R, 0.0, g, c0);
+  cell64_general(R, 0.0, g.re, g.vkm, TrigLib{}, c0);
   if (code == 0) code = c0.code;
 }
 
@@ -1299,9 +1594,6 @@ template <typename T>
 __host__ __device__ constexpr int grid_block() { return sizeof(T) == 4 ? SGP4B_BLOCK : SGP4B_BLOCK64; }
 constexpr int kGridMinBlocks = SGP4B_MINB;   // resident blocks per SM (fp32)
 
-__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
-__device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
-__device__ __forceinline__ void st_cs(int32_t* p, int32_t v) { __stcs(reinterpret_cast<int*>(p), (int)v); }
 
 // vector streaming stores / read-only loads of N consecutive elements
 template <int N>
@@ -1382,23 +1674,6 @@ __device__ __forceinline__ void compute_n(const RT& R, const float (&th)[kCellsP
     }
   }
 }
-
-template <bool LO, class RT>
-__device__ __forceinline__ void compute_cells(const RT& R, const double (&th)[kCellsPerLane],
-                                              const float (&)[kCellsPerLane], const Grav& g,
-                                              double (&out)[6][kCellsPerLane],
-                                              int (&code)[kCellsPerLane]) {
-  // fp64 cells are FP64-latency bound: SGP4B_F64_UNROLL cells interleave
-#pragma unroll kF64Unroll
-  for (int k = 0; k < kCellsPerLane; ++k) {
-    Cell64 c;
-    cell64(R, th[k], g, c);
-    out[0][k] = c.r[0]; out[1][k] = c.r[1]; out[2][k] = c.r[2];
-    out[3][k] = c.v[0]; out[4][k] = c.v[1]; out[5][k] = c.v[2];
-    code[k] = c.code;
-  }
-}
-
 
 // One satellite row, chunks [c0, c1): per lane kCellsPerLane consecutive
 // steps per chunk.  CellsFn(th, tl, out, code) evaluates a lane's cells;
@@ -1528,15 +1803,87 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t
   }
 }
 
-template <bool VEC, bool LO, class RT>
-__device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t c0, int64_t c1,
-                                             int lane, const double* times, const float* times_lo,
-                                             int64_t m, double* row, int64_t ps, int32_t* crow) {
-  auto cells = [&](const double (&th)[kCellsPerLane], const float (&tl)[kCellsPerLane],
-                   double (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
-    compute_cells<LO>(R, th, tl, g, out, code);
-  };
-  row_loop<double, VEC, LO>(cells, c0, c1, lane, times, times_lo, m, row, ps, crow);
+// fp64 row: lane l owns columns j0 + l + 32 k of each 128-column chunk, so
+// every cell is stored with fully coalesced 8-byte (4-byte code) streaming
+// stores straight from registers — no per-lane output buffer.  kIlp64 cells
+// (j, j + 32, ...) are evaluated per iteration: independent dependency
+// chains for the scheduler, and each record word read from shared memory
+// serves all of them.  FAST rows (Kepler class 1 by the record's ecco) run
+// cell64_c1 and hand a cell that leaves the class-1 domain to the
+// out-of-line general cell; other rows run the general cell.
+#ifndef SGP4B_F64_ILP
+#define SGP4B_F64_ILP 1
+#endif
+constexpr int kIlp64 = SGP4B_F64_ILP;
+
+template <bool FAST, bool ISIMP>
+__device__ __forceinline__ void row64(const RecS<double>& R, const TrigGrid& tr, double re,
+                                      double vkm, int64_t c0, int64_t c1, int lane,
+                                      const double* __restrict__ times, int64_t m,
+                                      double* __restrict__ row, int64_t ps,
+                                      int32_t* __restrict__ crow) {
+  // column indices are 32-bit (m < 2^31): one IMAD.WIDE per store address
+  // off the per-row plane bases
+  const unsigned jend = (unsigned)min(c1 * kCellsPerWarp, m);
+  double* const p0 = row;
+  double* const p1 = row + ps;
+  double* const p2 = row + 2 * ps;
+  double* const p3 = row + 3 * ps;
+  double* const p4 = row + 4 * ps;
+  double* const p5 = row + 5 * ps;
+#pragma unroll 1
+  for (unsigned j = (unsigned)(c0 * kCellsPerWarp) + lane; j < jend; j += 32 * kIlp64) {
+    double t[kIlp64];
+#pragma unroll
+    for (int i = 0; i < kIlp64; ++i) t[i] = j + 32 * i < jend ? __ldg(times + j + 32 * i) : 0.0;
+    Cell64 o[kIlp64];
+    bool ok[kIlp64];
+#pragma unroll
+    for (int i = 0; i < kIlp64; ++i) {
+      if constexpr (FAST) {
+        ok[i] = cell64_c1<ISIMP>(R, t[i], re, dbits(re), vkm, tr, o[i]);
+      } else {
+        cell64_general(R, t[i], re, vkm, tr, o[i]);
+        ok[i] = true;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kIlp64; ++i) {
+      const unsigned jj = j + 32 * i;
+      if (jj >= jend) break;
+      if (!ok[i]) {
+        cell64_fallback(R.p, t[i], re, vkm, tr.tab, row + jj, ps, crow + jj);
+        continue;
+      }
+#ifndef SGP4B_NOSTORE
+      st_cs(p0 + jj, o[i].r[0]);
+      st_cs(p1 + jj, o[i].r[1]);
+      st_cs(p2 + jj, o[i].r[2]);
+      st_cs(p3 + jj, o[i].v[0]);
+      st_cs(p4 + jj, o[i].v[1]);
+      st_cs(p5 + jj, o[i].v[2]);
+      st_cs(crow + jj, o[i].code);
+#else
+      if (o[i].r[0] + o[i].r[1] + o[i].v[2] == 1.2345e-300 && o[i].code == 77) st_cs(row + jj, o[i].r[0]);
+#endif
+    }
+  }
+}
+
+__device__ __forceinline__ void dispatch_row64(const RecS<double>& R, const TrigGrid& tr,
+                                               const Grav& g, int64_t c0, int64_t c1, int lane,
+                                               const double* times, int64_t m, double* row,
+                                               int64_t ps, int32_t* crow) {
+  const int flags = R.flags();
+  const bool fast = ((flags >> KEPLER_SHIFT) & 0xf) == 1;
+  if (fast) {
+    if (flags & FLAG_ISIMP)
+      row64<true, true>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+    else
+      row64<true, false>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+  } else {
+    row64<false, false>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+  }
 }
 
 // Persistent warps: the (satellite, chunk) work items of the grid are split
@@ -1573,10 +1920,20 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
   const int64_t g0 = total * w / nwarps;
   const int64_t g1 = total * (w + 1) / nwarps;
 
-  constexpr bool kSmem = sizeof(T) == 8 ? SGP4B_SMEM_REC64 : SGP4B_SMEM_REC;
+  constexpr bool kSmem = sizeof(T) == 8 ? true : SGP4B_SMEM_REC;   // fp64: records in smem
   constexpr bool kShfl = sizeof(T) == 4 && SGP4B_SHFL_REC;
   __shared__ __align__(16) T srec[kSmem ? kBlock / 32 : 1][S_COUNT];
   T* my = srec[kSmem ? (threadIdx.x >> 5) : 0];
+  // fp64: the (sin, cos)(2 pi i / 512) table of TrigTab, built per block
+  __shared__ double2 sintab[sizeof(T) == 8 ? kTabN : 1];
+  if constexpr (sizeof(T) == 8) {
+    for (int i = threadIdx.x; i < kTabN; i += kBlock) {
+      double sv, cv;
+      sincospi((double)i / (kTabN / 2), &sv, &cv);
+      sintab[i] = make_double2(sv, cv);
+    }
+    __syncthreads();
+  }
   using RecT = typename std::conditional<
       kShfl, RecW, typename std::conditional<kSmem, RecS<T>, Rec<T>>::type>::type;
   RecT R;
@@ -1611,9 +1968,14 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
     // pull the next row's record toward L1 while this row computes
     if (rec_idx == nullptr && gi + (c1 - c0) < g1 && lane < (int)(S_COUNT * sizeof(T) + 127) / 128)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (ri + 1) * S_COUNT + lane * (128 / sizeof(T))));
-    dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
-                     LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
-                     plane_stride, codes + sat * code_stride);
+    if constexpr (sizeof(T) == 8) {
+      dispatch_row64(R, TrigGrid{sintab}, g, c0, c1, lane, times + sat * times_ld, m,
+                     planes + sat * row_stride, plane_stride, codes + sat * code_stride);
+    } else {
+      dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
+                            LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
+                            plane_stride, codes + sat * code_stride);
+    }
     gi += c1 - c0;
 #ifdef SGP4B_TIMELINE
     if (first_row && lane == 0 && w < kTimelineWarps) {
@@ -1724,7 +2086,8 @@ int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* 
   if (slots <= 0) return fail(SGP4B_ECUDA, "%s: %s", what, g_last_error);
   if (blocks > slots) blocks = slots;
   if (precision == 64) {
-    auto k = vec ? grid_kernel<double, true, false> : grid_kernel<double, false, false>;
+    // fp64 rows store cell by cell (no vector path): one instance serves all
+    auto k = grid_kernel<double, true, false>;
     k<<<(unsigned)blocks, block, 0, s>>>(
         static_cast<const double*>(rec), rec_idx, n, static_cast<const double*>(times), nullptr,
         times_ld, m, g, static_cast<double*>(planes), plane_stride, row_stride, codes,
