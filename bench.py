@@ -374,8 +374,10 @@ def run_ours(args, world, rank, local) -> None:
         torch.sum(flush_r, 0, out=sink)
 
 
+    t_abs = float(np.max(np.abs(times)))
+
     def launch():
-        _device.propagate_grid(sats.device_satrec, t_dev, planes, error)
+        _device.propagate_grid(sats.device_satrec, t_dev, planes, error, t_absmax=t_abs)
 
     # the timed step replays a CUDA graph holding the grid-kernel launch (the
     # same kernel and arguments; the graph trims the per-launch CPU->GPU
@@ -432,7 +434,7 @@ def run_ours(args, world, rank, local) -> None:
 
     def init_and_launch():
         d = _device.init_device_tensor(el_dev, WGS72, precision, device)
-        _device.propagate_grid(d, t_dev, planes, error)
+        _device.propagate_grid(d, t_dev, planes, error, t_absmax=t_abs)
 
     ip_ms = []
     for k in range(max(3, min(args.steps, 10)) + 2):

@@ -78,21 +78,30 @@ int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev,
  *                 as the caller's fp64 time), or NULL; ignored for 64
  *   planes_dev : T base; plane p, row i, col j at
  *                planes_dev[p*plane_stride + i*row_stride + j]
- *   codes_dev  : int32 base; row i, col j at codes_dev[i*code_stride + j] */
+ *   codes_dev  : int32 base; row i, col j at codes_dev[i*code_stride + j]
+ *   t_absmax   : an upper bound on |times[j]| (minutes).  fp32 launches pick
+ *                each satellite's fixed-iteration Kepler class from ecco and
+ *                recompute the cells whose |t| could carry em out of that
+ *                class (drag over long or backward spans) with the general
+ *                path; the bound tells the kernel which rows can have such
+ *                cells.  INFINITY or NaN is always correct (every row of a
+ *                fixed class gets the check), only slower; fp64 ignores it. */
 int sgp4b_propagate_grid(const void* record_dev, int64_t n,
                          const void* times_dev, const float* times_lo_dev,
-                         int64_t m, int precision, const double* grav,
-                         void* planes_dev, int64_t plane_stride,
-                         int64_t row_stride, int32_t* codes_dev,
-                         int64_t code_stride, void* stream);
+                         int64_t m, double t_absmax, int precision,
+                         const double* grav, void* planes_dev,
+                         int64_t plane_stride, int64_t row_stride,
+                         int32_t* codes_dev, int64_t code_stride,
+                         void* stream);
 
 /* Elementwise pairs: cell k = satellite sat_idx[k] at times[k].  Replaces
  * the broadcasting scalar sgp4_propagate (kernel.py:513-534).
  *   rv_dev : (6, p) T out; codes_dev : (p) int32 out. */
 int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev,
                           const void* times_dev, const float* times_lo_dev,
-                          int64_t p, int precision, const double* grav,
-                          void* rv_dev, int32_t* codes_dev, void* stream);
+                          int64_t p, double t_absmax, int precision,
+                          const double* grav, void* rv_dev, int32_t* codes_dev,
+                          void* stream);
 
 /* fp32-vs-fp64 drift: per-cell |r32 - r64| (km) and |v32 - v64| (km/s) in
  * fp64 for cells whose codes are 0 in both grids, +inf elsewhere.  Both

@@ -143,15 +143,28 @@ def pack_device(satrec64: np.ndarray, codes: np.ndarray, isimp: np.ndarray,
     return DeviceSatrec(sr, cd, si, record, precision, grav, device)
 
 
+def times_absmax(times) -> float:
+    """max |t| of a time vector (host array or device tensor; a device
+    tensor costs one reduction and a sync)."""
+    if isinstance(times, torch.Tensor):
+        return float(times.detach().abs().max().item()) if times.numel() else 0.0
+    t = np.asarray(times)
+    return float(np.max(np.abs(t))) if t.size else 0.0
+
+
 def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,
                    codes: torch.Tensor, times_lo: torch.Tensor | None = None,
-                   rows: tuple[int, int] | None = None) -> None:
+                   rows: tuple[int, int] | None = None, t_absmax: float | None = None) -> None:
     """Launch the grid kernel: planes (6, n, m) and codes (n, m) device
     tensors (any strides with unit column stride) receive the grid.
 
     ``rows=(r0, r1)`` propagates only satellites r0..r1 into row 0.. of the
-    outputs (used by tiling and by the streamed API).
+    outputs (used by tiling and by the streamed API).  ``t_absmax`` is an
+    upper bound on |times| (fp32 Kepler-class validity, see sgp4b.h); it is
+    computed from ``times`` when not given.
     """
+    if t_absmax is None:
+        t_absmax = times_absmax(times) if dev.precision == 32 else float("inf")
     r0, r1 = rows if rows is not None else (0, dev.n)
     n = r1 - r0
     m = int(times.shape[0])
@@ -160,17 +173,20 @@ def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,
     rec = dev.record[r0:r1]
     g = _grav_host(dev.grav, dev.device)
     _native.check(_native.load().sgp4b_propagate_grid(
-        rec.data_ptr(), n, times.data_ptr(), _native.ptr(times_lo), m, dev.precision,
+        rec.data_ptr(), n, times.data_ptr(), _native.ptr(times_lo), m, float(t_absmax),
+        dev.precision,
         _host_ptr(g), planes.data_ptr(), planes.stride(0), planes.stride(1),
         codes.data_ptr(), codes.stride(0), _stream(dev.device)))
 
 
 def propagate_pairs(dev: DeviceSatrec, sat_idx: torch.Tensor, times: torch.Tensor,
-                    rv: torch.Tensor, codes: torch.Tensor) -> None:
+                    rv: torch.Tensor, codes: torch.Tensor, t_absmax: float | None = None) -> None:
     p = int(times.shape[0])
     g = _grav_host(dev.grav, dev.device)
+    if t_absmax is None:
+        t_absmax = times_absmax(times) if dev.precision == 32 else float("inf")
     _native.check(_native.load().sgp4b_propagate_pairs(
-        dev.record.data_ptr(), sat_idx.data_ptr(), times.data_ptr(), None, p,
+        dev.record.data_ptr(), sat_idx.data_ptr(), times.data_ptr(), None, p, float(t_absmax),
         dev.precision, _host_ptr(g), rv.data_ptr(), codes.data_ptr(),
         _stream(dev.device)))
 

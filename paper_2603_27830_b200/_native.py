@@ -16,7 +16,7 @@ LIB_PATH = _HERE / LIB_NAME
 
 SATREC_FIELDS = 33
 RECORD_SLOTS = 40
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 #: every symbol include/sgp4b.h declares, in header order
 EXPORTED_SYMBOLS = (
@@ -39,10 +39,10 @@ _vp = ctypes.c_void_p
 _SIGNATURES = {
     "sgp4b_init": (_c_int, [_vp, _c_i64, _vp, _c_int, _vp, _vp, _vp, _vp, _vp]),
     "sgp4b_pack": (_c_int, [_vp, _vp, _vp, _c_i64, _vp, _c_int, _vp, _vp]),
-    "sgp4b_propagate_grid": (_c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _c_int, _vp,
-                                      _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
-    "sgp4b_propagate_pairs": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp,
-                                       _vp, _vp, _vp]),
+    "sgp4b_propagate_grid": (_c_int, [_vp, _c_i64, _vp, _vp, _c_i64, ctypes.c_double, _c_int,
+                                      _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
+    "sgp4b_propagate_pairs": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, ctypes.c_double, _c_int,
+                                       _vp, _vp, _vp, _vp]),
     "sgp4b_drift_norms": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
     "sgp4b_solve_kepler": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _vp, _vp]),
     "sgp4b_host_alloc": (_c_int, [_c_i64, ctypes.POINTER(_vp)]),

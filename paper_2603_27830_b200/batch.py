@@ -180,13 +180,15 @@ def _alloc_grid(n: int, m: int, precision: int, device, pin: bool = False):
 
 
 def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
-                           times_lo=None) -> BatchResult:
+                           times_lo=None, t_absmax: float | None = None) -> BatchResult:
     """Propagate every satellite to every time, leaving the grid in HBM.
 
     ``times`` is a 1-D array/tensor (cast to the batch dtype); ``out`` may
     supply preallocated (planes, error) device tensors.  ``times_lo``
     (fp32 batches only) carries the low words of fp64 times for the
-    double-float secular stage.  Returns a BatchResult of torch tensors.
+    double-float secular stage.  ``t_absmax`` may give max |times| when the
+    caller knows it (device-tensor times are otherwise reduced on the device,
+    one sync).  Returns a BatchResult of torch tensors.
     """
     dev = sats.device_satrec
     with torch.cuda.device(dev.device):
@@ -195,7 +197,10 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
             if t_d.ndim != 1 or t_d.numel() == 0:
                 raise ValueError("times must be a non-empty 1-D array")
         else:
-            t_d = torch.from_numpy(_times(sats, times)).to(dev.device)
+            t_h = _times(sats, times)
+            if t_absmax is None:
+                t_absmax = _device.times_absmax(t_h)
+            t_d = torch.from_numpy(t_h).to(dev.device)
         t_d = t_d.contiguous()
         if t_d.data_ptr() % 16:              # the vector path wants 16-B aligned times
             t_d = t_d.clone()
@@ -206,7 +211,7 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
             planes, error = _alloc_grid(sats.n, m, dev.precision, dev.device)
         else:
             planes, error = _check_out(out, sats.n, m, dev.precision, dev.device)
-        _device.propagate_grid(dev, t_d, planes, error, times_lo=times_lo)
+        _device.propagate_grid(dev, t_d, planes, error, times_lo=times_lo, t_absmax=t_absmax)
     return BatchResult(planes=planes, error=error, n=sats.n, m=m)
 
 
@@ -276,7 +281,7 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchR
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
         t_d = torch.from_numpy(t).to(dev.device, non_blocking=True)
-        res = propagate_batch_device(sats, t_d)
+        res = propagate_batch_device(sats, t_d, t_absmax=_device.times_absmax(t))
         torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
         torch.from_numpy(error_h).copy_(res.error, non_blocking=True)
         stream.synchronize()
@@ -341,13 +346,14 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
         t_d = torch.from_numpy(t).to(dev.device)
+        t_abs = _device.times_absmax(t)
 
         def launch(tile):
             rows, cols = tile
             tr, tc = rows.stop - rows.start, cols.stop - cols.start
             planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
             _device.propagate_grid(dev, t_d[cols].clone(), planes_d, err_d,
-                                   rows=(rows.start, rows.stop))
+                                   rows=(rows.start, rows.stop), t_absmax=t_abs)
             planes_h, err_h = _host_grid(tr, tc, dev.precision)
             torch.from_numpy(planes_h).copy_(planes_d, non_blocking=True)
             torch.from_numpy(err_h).copy_(err_d, non_blocking=True)

@@ -1022,7 +1022,7 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   // without cancelling against u.
   V2 s, c, d = sp<NC>(0.0f), tem5 = sp<NC>(0.0f);
   V2 eo1 = u;
-  const int kiter = KITER > 0 ? KITER : ((flags >> KEPLER_SHIFT) & 0xf);
+  const int kiter = KITER > 0 ? KITER : 10;     // the reference loop bound
 #pragma unroll
   for (int it = 0; it < (KITER > 0 ? KITER : 16); ++it) {
     if (KITER == 0 && it >= kiter) break;
@@ -1678,12 +1678,14 @@ __device__ __forceinline__ void compute_n(const RT& R, const float (&th)[kCellsP
 // One satellite row, chunks [c0, c1): per lane kCellsPerLane consecutive
 // steps per chunk.  CellsFn(th, tl, out, code) evaluates a lane's cells;
 // it is specialised per satellite class, so the chunk loop is branch-free.
-template <typename T, bool VEC, bool LO, class CellsFn>
+// MASKED: store only the cells with |t| > t_crit (the general instance's
+// second pass over a row, see dispatch_row).
+template <typename T, bool VEC, bool LO, bool MASKED, class CellsFn>
 __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64_t c1, int lane,
                                          const T* __restrict__ times,
                                          const float* __restrict__ times_lo, int64_t m,
                                          T* __restrict__ row, int64_t plane_stride,
-                                         int32_t* __restrict__ crow) {
+                                         int32_t* __restrict__ crow, float t_crit) {
   // a lane's kCellsPerLane times at column j (zero past the row end)
   auto load_times = [&](int64_t j, T (&th)[kCellsPerLane], float (&tl)[kCellsPerLane]) {
     if (VEC && j + kCellsPerLane <= m) {
@@ -1719,6 +1721,24 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     T out[6][kCellsPerLane];
     int code[kCellsPerLane];
     cells(th, tl, out, code);
+    if constexpr (MASKED) {
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) {
+        if (fabsf((float)th[k]) > t_crit && j0 + k < m) {
+#pragma unroll
+          for (int p = 0; p < 6; ++p) st_cs(pb + p * plane_stride + k, out[p][k]);
+          st_cs(cb + k, code[k]);
+        }
+      }
+      pb += kCellsPerWarp;
+      cb += kCellsPerWarp;
+#pragma unroll
+      for (int k = 0; k < kCellsPerLane; ++k) {
+        th[k] = thn[k];
+        tl[k] = tln[k];
+      }
+      continue;
+    }
 #ifdef SGP4B_NOSTORE
     // analysis build: compute-only timing (results kept alive, never stored)
     {
@@ -1766,40 +1786,86 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
   }
 }
 
-template <bool ISIMP, int KITER, bool VEC, bool LO, class RT>
-__device__ __forceinline__ void row32(const RT& R, const Grav& g, int64_t c0, int64_t c1, int lane,
-                                      const float* times, const float* times_lo, int64_t m,
-                                      float* row, int64_t plane_stride, int32_t* crow) {
+template <bool ISIMP, int KITER, bool VEC, bool LO, bool MASKED = false, class RT>
+__device__ __forceinline__ void row32(const RT& R, const Grav& g, int64_t c0, int64_t c1,
+                                      int lane, const float* times, const float* times_lo,
+                                      int64_t m, float* row, int64_t plane_stride, int32_t* crow,
+                                      float t_crit) {
   auto cells = [&](const float (&th)[kCellsPerLane], const float (&tl)[kCellsPerLane],
                    float (&out)[6][kCellsPerLane], int (&code)[kCellsPerLane]) {
     compute_n<ISIMP, KITER, LO>(R, th, tl, g, out, code);
   };
-  row_loop<float, VEC, LO>(cells, c0, c1, lane, times, times_lo, m, row, plane_stride, crow);
+  row_loop<float, VEC, LO, MASKED>(cells, c0, c1, lane, times, times_lo, m, row, plane_stride,
+                                   crow, t_crit);
 }
 
-// per-row dispatch on the satellite's (isimp, Kepler count): warp-uniform
+// The masked general pass over one row, out of line (rarely executed; kept
+// out of the class passes' register allocation): reloads the record.
+template <bool ISIMP, bool VEC, bool LO>
+__device__ __noinline__ void fixup_row(const float* recg, float re_f, float vkm_f, int64_t c0,
+                                       int64_t c1, int lane, const float* times,
+                                       const float* times_lo, int64_t m, float* row, int64_t ps,
+                                       int32_t* crow, float t_crit) {
+  Rec<float> R;
+  load_rec(recg, R);
+  Grav g{};
+  g.re_f = re_f;
+  g.vkm_f = vkm_f;
+  row32<ISIMP, 0, VEC, LO, true>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow, t_crit);
+}
+
+// Per-row dispatch on the satellite's (isimp, Kepler class): warp-uniform.
+// The class was chosen from ecco at init (kepler_iters_for); it stays valid
+// while |em| = |ecco + bc5 sinmao - bc4 t - bc5 sin mm| is below the class
+// bound, which holds for |t| <= t_crit = (bound - |E0| - 2 |bc5|) / |bc4|.
+// t_absmax (launch argument) bounds |t| over the launch; when it exceeds a
+// row's t_crit (long or backward spans of high-drag objects) the cells
+// beyond t_crit are recomputed by the general instance in a second, masked
+// pass over the row, so every cell's value is a function of its own
+// (satellite, t) only (batch == scalar).
 template <bool VEC, bool LO, class RT>
-__device__ __forceinline__ void dispatch_row(const RT& R, const Grav& g, int64_t c0, int64_t c1,
-                                             int lane, const float* times, const float* times_lo,
-                                             int64_t m, float* row, int64_t ps, int32_t* crow) {
+__device__ __forceinline__ void dispatch_row(const RT& R, const float* recg, const Grav& g,
+                                             int64_t c0, int64_t c1, int lane, const float* times,
+                                             const float* times_lo, int64_t m, float* row,
+                                             int64_t ps, int32_t* crow, float t_absmax) {
 #ifdef SGP4B_ONLY_CLASS_K1
   // analysis build: every row runs the (non-isimp, Kepler SGP4B_ONLY_CLASS_K1)
   // instance, so the SASS holds one chunk loop (static instruction mix)
-  row32<false, SGP4B_ONLY_CLASS_K1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  row32<false, SGP4B_ONLY_CLASS_K1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow,
+                                             INFINITY);
   return;
 #endif
   const int flags = R.flags();
   const int kit = (flags >> KEPLER_SHIFT) & 0xf;
-  if (!(flags & FLAG_ISIMP)) {
-    if (kit == 1) row32<false, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else if (kit == 2) row32<false, 2, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else if (kit == 3) row32<false, 3, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else row32<false, 0, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+  const bool simp = flags & FLAG_ISIMP;
+  auto t_crit_of = [&](const auto& rec) {
+    const float bound = kit == 1 ? 0.004f : kit == 2 ? 0.1f : 0.4f;
+    const float slack = bound - fabsf(rec[P_E0]) - 2.0f * fabsf(rec[P_BC5]);
+    return slack > 0.0f ? slack / fabsf(rec[P_BC4]) : -1.0f;
+  };
+  // NaN t_absmax (unknown bound) counts as unbounded
+  const bool need = kit >= 1 && kit <= 3 && !(t_absmax <= t_crit_of(R));
+#define SGP4B_ROW(S, K) row32<S, K, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow, INFINITY)
+  if (!simp) {
+    if (kit == 1) SGP4B_ROW(false, 1);
+    else if (kit == 2) SGP4B_ROW(false, 2);
+    else if (kit == 3) SGP4B_ROW(false, 3);
+    else SGP4B_ROW(false, 0);
   } else {
-    if (kit == 1) row32<true, 1, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else if (kit == 2) row32<true, 2, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else if (kit == 3) row32<true, 3, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
-    else row32<true, 0, VEC, LO>(R, g, c0, c1, lane, times, times_lo, m, row, ps, crow);
+    if (kit == 1) SGP4B_ROW(true, 1);
+    else if (kit == 2) SGP4B_ROW(true, 2);
+    else if (kit == 3) SGP4B_ROW(true, 3);
+    else SGP4B_ROW(true, 0);
+  }
+#undef SGP4B_ROW
+  if (need) {
+    const float t_crit = t_crit_of(R);
+    if (!simp)
+      fixup_row<false, VEC, LO>(recg, g.re_f, g.vkm_f, c0, c1, lane, times, times_lo, m, row, ps,
+                                crow, t_crit);
+    else
+      fixup_row<true, VEC, LO>(recg, g.re_f, g.vkm_f, c0, c1, lane, times, times_lo, m, row, ps,
+                               crow, t_crit);
   }
 }
 
@@ -1911,7 +1977,7 @@ __global__ void __launch_bounds__(grid_block<T>(), sizeof(T) == 4 ? kGridMinBloc
 grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t n,
             const T* __restrict__ times, const float* __restrict__ times_lo, int64_t times_ld,
             int64_t m, Grav g, T* __restrict__ planes, int64_t plane_stride, int64_t row_stride,
-            int32_t* __restrict__ codes, int64_t code_stride, int64_t chunks) {
+            int32_t* __restrict__ codes, int64_t code_stride, int64_t chunks, float t_absmax) {
   constexpr int kBlock = grid_block<T>();
   const int64_t nwarps = (int64_t)gridDim.x * (kBlock / 32);
   const int64_t w = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -1972,9 +2038,10 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
       dispatch_row64(R, TrigGrid{sintab}, g, c0, c1, lane, times + sat * times_ld, m,
                      planes + sat * row_stride, plane_stride, codes + sat * code_stride);
     } else {
-      dispatch_row<VEC, LO>(R, g, c0, c1, lane, times + sat * times_ld,
+      dispatch_row<VEC, LO>(R, reinterpret_cast<const float*>(rec) + ri * S_COUNT, g, c0, c1,
+                            lane, times + sat * times_ld,
                             LO ? times_lo + sat * times_ld : nullptr, m, planes + sat * row_stride,
-                            plane_stride, codes + sat * code_stride);
+                            plane_stride, codes + sat * code_stride, t_absmax);
     }
     gi += c1 - c0;
 #ifdef SGP4B_TIMELINE
@@ -2077,7 +2144,10 @@ int64_t resident_blocks(int precision) {
 int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* times,
                 const float* times_lo, int64_t times_ld, int64_t m, int precision, const Grav& g,
                 void* planes, int64_t plane_stride, int64_t row_stride, int32_t* codes,
-                int64_t code_stride, bool vec, cudaStream_t s, const char* what) {
+                int64_t code_stride, bool vec, double t_absmax, cudaStream_t s, const char* what) {
+  // an upper bound on |t|, rounded up into fp32 (NaN stays NaN: unbounded)
+  float tb = (float)t_absmax;
+  if ((double)tb < t_absmax) tb = nextafterf(tb, INFINITY);
   const int64_t chunks = (m + kCellsPerWarp - 1) / kCellsPerWarp;
   const int64_t warps = n * chunks;
   const int block = precision == 64 ? grid_block<double>() : grid_block<float>();
@@ -2091,7 +2161,7 @@ int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* 
     k<<<(unsigned)blocks, block, 0, s>>>(
         static_cast<const double*>(rec), rec_idx, n, static_cast<const double*>(times), nullptr,
         times_ld, m, g, static_cast<double*>(planes), plane_stride, row_stride, codes,
-        code_stride, chunks);
+        code_stride, chunks, tb);
   } else {
     auto k = times_lo != nullptr
                  ? (vec ? grid_kernel<float, true, true> : grid_kernel<float, false, true>)
@@ -2099,7 +2169,7 @@ int launch_grid(const void* rec, const int64_t* rec_idx, int64_t n, const void* 
     k<<<(unsigned)blocks, block, 0, s>>>(
         static_cast<const float*>(rec), rec_idx, n, static_cast<const float*>(times), times_lo,
         times_ld, m, g, static_cast<float*>(planes), plane_stride, row_stride, codes, code_stride,
-        chunks);
+        chunks, tb);
   }
   return check_launch(what);
 }
@@ -2113,7 +2183,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 2; }
+int sgp4b_abi_version(void) { return 3; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -2154,9 +2224,10 @@ int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev, const uin
 }
 
 int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_dev,
-                         const float* times_lo_dev, int64_t m, int precision, const double* grav,
-                         void* planes_dev, int64_t plane_stride, int64_t row_stride,
-                         int32_t* codes_dev, int64_t code_stride, void* stream) {
+                         const float* times_lo_dev, int64_t m, double t_absmax, int precision,
+                         const double* grav, void* planes_dev, int64_t plane_stride,
+                         int64_t row_stride, int32_t* codes_dev, int64_t code_stride,
+                         void* stream) {
   Grav g;
   if (n <= 0 || m <= 0)
     return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: empty grid (%lld x %lld)", (long long)n,
@@ -2172,13 +2243,13 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_de
                    ((uintptr_t)planes_dev % (4 * esz) == 0) && ((uintptr_t)codes_dev % 16 == 0) &&
                    ((uintptr_t)times_dev % (4 * esz) == 0);
   return launch_grid(record_dev, nullptr, n, times_dev, times_lo_dev, 0, m, precision, g,
-                     planes_dev, plane_stride, row_stride, codes_dev, code_stride, vec,
+                     planes_dev, plane_stride, row_stride, codes_dev, code_stride, vec, t_absmax,
                      (cudaStream_t)stream, "sgp4b_propagate_grid");
 }
 
 int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, const void* times_dev,
-                          const float* times_lo_dev, int64_t p, int precision, const double* grav,
-                          void* rv_dev, int32_t* codes_dev, void* stream) {
+                          const float* times_lo_dev, int64_t p, double t_absmax, int precision,
+                          const double* grav, void* rv_dev, int32_t* codes_dev, void* stream) {
   Grav g;
   if (p <= 0) return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: p must be positive");
   if (precision != 32 && precision != 64)
@@ -2189,7 +2260,7 @@ int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, co
   // The VEC instance (m = 1 never takes its vector path) is the one aligned
   // grids use, so a pair equals the corresponding grid cell bit for bit.
   return launch_grid(record_dev, sat_idx_dev, p, times_dev, times_lo_dev, 1, 1, precision, g,
-                     rv_dev, p, 1, codes_dev, 1, true, (cudaStream_t)stream,
+                     rv_dev, p, 1, codes_dev, 1, true, t_absmax, (cudaStream_t)stream,
                      "sgp4b_propagate_pairs");
 }
 

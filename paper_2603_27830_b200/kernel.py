@@ -217,7 +217,7 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
         t_d = torch.from_numpy(tt).to(device)
         rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
         codes = torch.empty((p,), dtype=torch.int32, device=device)
-        _device.propagate_pairs(dev, idx_d, t_d, rv, codes)
+        _device.propagate_pairs(dev, idx_d, t_d, rv, codes, t_absmax=_device.times_absmax(tt))
         rv_h = rv.cpu().numpy()
         codes_h = codes.cpu().numpy()
     r[...] = rv_h[:3].T.reshape(out_shape + (3,))
@@ -236,7 +236,7 @@ def _grid_of_rows(dev, rows: np.ndarray, times: np.ndarray):
                               codes=dev.codes.index_select(0, rows_d))
     t_d = torch.from_numpy(np.array(times)).to(device)
     planes, codes = _alloc_grid(int(rows.size), int(times.size), dev.precision, device)
-    _device.propagate_grid(sub, t_d, planes, codes)
+    _device.propagate_grid(sub, t_d, planes, codes, t_absmax=_device.times_absmax(times))
     return planes, codes
 
 

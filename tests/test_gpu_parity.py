@@ -744,3 +744,73 @@ def test_extreme_grid_shapes(oracle, corpus_columns, n, m):
     ok = ref_c == 0
     dr = np.linalg.norm(got[:3].T[ok].astype(np.float64) - ref_r[ok], axis=1)
     assert dr.max() < 0.5
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_kepler_class_leaves_domain(oracle, corpus_columns, precision):
+    """A near-circular satellite (fast Kepler class by its ecco) with heavy
+    drag propagated far backward and forward, so em = ecco - bstar cc4 t - ...
+    leaves the class's domain inside one row: the cells beyond it must take
+    the general path (fp32: the masked second pass; fp64: the per-cell
+    fallback).  Codes equal the reference, states stay within the bars, and
+    every cell equals the scalar API's value for the same (satellite, t)."""
+    pkg = _gpu()
+    base = corpus_columns[:, [137, 415, 391]].copy()   # the corpus's largest bstar*cc4
+    base[1] = 0.0029                                   # class 1 (e + 0.001 < 0.004)
+    base[6] = [1e-2, -1e-2, 1e-2]                      # heavy drag, both signs
+    times = np.linspace(-20160.0, 20160.0, 257)
+    ref64, codes64 = oracle.grid(oracle.init_columns(base, 64), times)
+    _, codes32 = oracle.grid(oracle.init_columns(base, 32), times)
+    sats = pkg.init_batch(base, precision=precision)
+    res = pkg.propagate_batch(sats, times)
+    assert np.array_equal(res.error, codes64)
+    if precision == 32:
+        assert np.array_equal(res.error, codes32)
+    ok = codes64 == 0
+    # the class domain (|em| < 0.004) is really left on code-0 cells:
+    # |t| beyond t_crit = (0.004 - e - 2|bstar cc5|) / |bstar cc4|
+    init64 = oracle.init_columns(base, 64)
+    bc4 = np.abs(np.asarray(init64["bstar"]) * np.asarray(init64["cc4"]))
+    bc5 = np.abs(np.asarray(init64["bstar"]) * np.asarray(init64["cc5"]))
+    t_crit = (0.004 - base[1] - 2 * bc5) / bc4
+    assert (ok & (np.abs(times)[None, :] > t_crit[:, None])).any(axis=1).all()
+    # backward propagation with this much drag inflates the orbit to |r| ~
+    # 1e8 km, where the 1 mm bar is below fp64 resolution: there the bar is
+    # relative (1e-10 |r|), and the absolute bars apply to |r| < 5e4 km
+    rad = np.linalg.norm(ref64[:3], axis=0)
+    far = ok & (rad >= 5e4)
+    if precision == 64 and far.any():
+        drf = np.linalg.norm(res.planes[:3] - ref64[:3], axis=0)[far]
+        assert (drf <= 1e-10 * rad[far]).all()
+    ok &= rad < 5e4
+    dr, dv = _diff(res.planes, ref64, ok)
+    print(f"\nclass-domain fp{precision}: ok cells {int(ok.sum())}, max|dr| {dr.max() * 1e3:.3f} m")
+    if precision == 64:
+        assert dr.max() <= TOL64_R and dv.max() <= TOL64_V
+    else:
+        ref32, _ = oracle.grid(oracle.init_columns(base, 32), times)
+        dr_ref, _ = _diff(ref32, ref64, ok)
+        assert dr.max() <= dr_ref.max() + 0.05
+    dtype = np.float32 if precision == 32 else np.float64
+    st = pkg.sgp4_propagate(sats.init, times.astype(dtype)[:, None])
+    assert np.array_equal(np.transpose(st.r, (2, 1, 0)), res.planes[:3], equal_nan=True)
+    assert np.array_equal(np.transpose(st.v, (2, 1, 0)), res.planes[3:], equal_nan=True)
+
+
+def test_t_absmax_bound_only_changes_speed(corpus_columns):
+    """t_absmax only selects which rows get the masked general pass: an
+    unknown (inf / NaN) bound gives the same grid bit for bit."""
+    import torch
+    from paper_2603_27830_b200 import _device
+    from paper_2603_27830_b200.batch import _alloc_grid
+    pkg = _gpu()
+    cols = corpus_columns[:, :64].copy()
+    cols[6, ::3] = 5e-3
+    sats = pkg.init_batch(cols, precision=32)
+    times = np.linspace(-20160.0, 20160.0, 129)
+    ref = pkg.propagate_batch_device(sats, times)
+    t_d = torch.from_numpy(times.astype(np.float32)).cuda()
+    for bound in (float("inf"), float("nan"), 1e30):
+        planes, codes = _alloc_grid(64, 129, 32, t_d.device)
+        _device.propagate_grid(sats.device_satrec, t_d, planes, codes, t_absmax=bound)
+        assert torch.equal(planes, ref.planes) and torch.equal(codes, ref.error)
