@@ -17,6 +17,7 @@ from .gravity import GravityModel
 
 SATREC_FIELDS = _native.SATREC_FIELDS
 RECORD_SLOTS = _native.RECORD_SLOTS
+MAX_INIT_CODE = (1 << 23) - 1        # width of the record's persistent-code field
 
 
 def require_cuda(device=None) -> torch.device:
@@ -128,6 +129,13 @@ def init_device_tensor(el: torch.Tensor, grav: GravityModel, precision: int,
 def pack_device(satrec64: np.ndarray, codes: np.ndarray, isimp: np.ndarray,
                 grav: GravityModel, precision: int, device=None) -> DeviceSatrec:
     """Host SoA fields (e.g. from a user-built SatInit) -> packed records."""
+    codes_i = np.asarray(codes)
+    if codes_i.size and (codes_i.min() < 0 or codes_i.max() > MAX_INIT_CODE):
+        # the packed record carries the persistent code in 23 bits; the
+        # reference keeps any nonzero code, so out-of-range ones are refused
+        # rather than silently wrapped to another value
+        raise ValueError(f"error_code_at_init must be in [0, {MAX_INIT_CODE}], got "
+                         f"[{int(codes_i.min())}, {int(codes_i.max())}]")
     device = require_cuda(device)
     n = satrec64.shape[1]
     # np.array copies: the SatInit fields may be read-only views

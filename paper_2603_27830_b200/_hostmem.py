@@ -16,6 +16,7 @@ GPU of the process can DMA into it.
 from __future__ import annotations
 
 import atexit
+import collections
 import ctypes
 import os
 import threading
@@ -30,6 +31,11 @@ _DEFAULT_LIMIT = 4 << 30
 
 _lock = threading.Lock()
 _free: list[tuple[int, int]] = []          # (size, ptr) of retained free blocks
+# blocks released by PinnedBlock.__del__: a finalizer may run inside any
+# allocation (GC), even while this module holds _lock, so it never takes the
+# lock; it appends here (deque.append is atomic) and the next pool call
+# drains the queue under the lock
+_released: collections.deque = collections.deque()
 _stats = {"pinned_bytes": 0, "cached_bytes": 0, "allocs": 0, "reuses": 0}
 
 
@@ -62,19 +68,25 @@ class PinnedBlock:
 
     def __del__(self):
         if self.ptr:
-            _give_back(self.ptr, self.size)
+            _released.append((self.size, self.ptr))
             self.ptr = 0
 
 
-def _give_back(ptr: int, size: int) -> None:
-    with _lock:
-        if _stats["cached_bytes"] + size <= cache_limit():
+def _drain() -> list[int]:
+    """Move released blocks into the free list (caller holds _lock); returns
+    the pointers beyond the cache limit, to be unpinned outside the lock."""
+    excess = []
+    limit = cache_limit()
+    while _released:
+        size, ptr = _released.popleft()
+        if _stats["cached_bytes"] + size <= limit:
             _free.append((size, ptr))
-            _free.sort()
             _stats["cached_bytes"] += size
-            return
-        _stats["pinned_bytes"] -= size
-    _free_ptr(ptr)
+        else:
+            _stats["pinned_bytes"] -= size
+            excess.append(ptr)
+    _free.sort()
+    return excess
 
 
 def _free_ptr(ptr: int) -> None:
@@ -88,13 +100,20 @@ def alloc(nbytes: int) -> PinnedBlock:
     """A pinned block of at least ``nbytes`` (reused from the pool when a free
     block is no more than 1.5x the rounded request)."""
     size = _round(max(int(nbytes), 1))
+    hit = None
     with _lock:
+        excess = _drain()
         for k, (sz, ptr) in enumerate(_free):
             if sz >= size and sz <= size + size // 2:
                 del _free[k]
                 _stats["cached_bytes"] -= sz
                 _stats["reuses"] += 1
-                return PinnedBlock(ptr, sz)
+                hit = (ptr, sz)
+                break
+    for ptr in excess:
+        _free_ptr(ptr)
+    if hit is not None:
+        return PinnedBlock(*hit)
     lib = _native.load()
     out = ctypes.c_void_p()
     status = lib.sgp4b_host_alloc(size, ctypes.byref(out))
@@ -128,18 +147,23 @@ def empty(shapes_dtypes) -> list[np.ndarray]:
 def empty_cache() -> None:
     """Unpin and free every retained free block."""
     with _lock:
+        excess = _drain()
         blocks = list(_free)
         _free.clear()
         _stats["cached_bytes"] = 0
         _stats["pinned_bytes"] -= sum(s for s, _ in blocks)
-    for _, ptr in blocks:
+    for ptr in excess + [p for _, p in blocks]:
         _free_ptr(ptr)
 
 
 def stats() -> dict:
     """pinned_bytes (live + cached), cached_bytes (free, retained), allocs, reuses."""
     with _lock:
-        return dict(_stats)
+        excess = _drain()
+        out = dict(_stats)
+    for ptr in excess:
+        _free_ptr(ptr)
+    return out
 
 
 atexit.register(empty_cache)

@@ -264,7 +264,74 @@ def split_times(times) -> tuple[np.ndarray, np.ndarray]:
     return hi, lo
 
 
-def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchResult:
+def _shard_satrec(dev: "_device.DeviceSatrec", lo: int, hi: int, device) -> "_device.DeviceSatrec":
+    """Rows lo..hi of a batch's packed records on ``device`` (a peer copy
+    over NVLink when it is another GPU; 160/320 bytes per satellite)."""
+    rec = dev.record[lo:hi]
+    codes = dev.codes[lo:hi]
+    if torch.device(device) != dev.device:
+        rec = rec.to(device, non_blocking=True)
+        codes = codes.to(device, non_blocking=True)
+    return _device.DeviceSatrec(satrec=None, codes=codes, isimp=None, record=rec,
+                                precision=dev.precision, grav=dev.grav,
+                                device=torch.device(device))
+
+
+def _devices(devices) -> list:
+    out = []
+    for d in devices:
+        d = torch.device("cuda", d) if isinstance(d, int) else torch.device(d)
+        out.append(_device.require_cuda(d))
+    if not out:
+        raise ValueError("devices must name at least one CUDA device")
+    return out
+
+
+def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
+    """``propagate_batch`` over several GPUs of this process (reference
+    batch.py:125-141, 193-204: the grid is partitioned into balanced
+    satellite ranges, ``partition_work``'s rule, and computed concurrently).
+
+    Each device gets its rows' packed records (peer copy), runs the grid
+    kernel on its own stream, and copies its rows straight into one pinned
+    host grid over its own PCIe link, so the D2H — the bound of the
+    single-GPU path — runs on all links at once.  Cells are bitwise equal to
+    the single-device result (no collective, satellites are independent).
+    """
+    t = _times(sats, times)
+    dev = sats.device_satrec
+    n, m = sats.n, t.size
+    devs = _devices(devices)
+    planes_h, error_h = _host_grid(n, m, dev.precision)
+    t_abs = _device.times_absmax(t)
+    src_stream = torch.cuda.current_stream(dev.device)
+    ready = torch.cuda.Event()
+    ready.record(src_stream)                  # the records exist on the source device
+    jobs = []
+    from .shard import shard_bounds
+    for g, d in enumerate(devs):
+        lo, hi = shard_bounds(n, len(devs), g)
+        if hi <= lo:
+            continue
+        with torch.cuda.device(d):
+            stream = torch.cuda.Stream(d)
+            stream.wait_event(ready)
+            with torch.cuda.stream(stream):
+                sub = _shard_satrec(dev, lo, hi, d)
+                t_d = torch.from_numpy(t).to(d, non_blocking=True)
+                planes, error = _alloc_grid(hi - lo, m, dev.precision, d)
+                _device.propagate_grid(sub, t_d, planes, error, t_absmax=t_abs)
+                for p in range(6):
+                    torch.from_numpy(planes_h[p, lo:hi]).copy_(planes[p], non_blocking=True)
+                torch.from_numpy(error_h[lo:hi]).copy_(error, non_blocking=True)
+            jobs.append((stream, sub, t_d, planes, error))
+    for stream, *_ in jobs:
+        stream.synchronize()
+    return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
+
+
+def propagate_batch(sats: SatBatch, times, workers: int | None = None,
+                    devices=None) -> BatchResult:
     """Propagate every satellite to every time (batch.py:166-205).
 
     Cell (i, j) is bitwise equal to ``sgp4_propagate`` of satellite i at
@@ -273,7 +340,11 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None) -> BatchR
     Returns numpy arrays, fully materialised: the planes and the int32 code
     plane are copied from HBM into one page-locked host block (pooled at its
     exact size, see ``_hostmem``) that is released with the arrays.
+    ``devices`` (e.g. ``range(torch.cuda.device_count())``) spreads the
+    satellites over several GPUs of this process (``propagate_batch_multi``).
     """
+    if devices is not None and len(list(devices)) > 0:
+        return propagate_batch_multi(sats, times, devices)
     t = _times(sats, times)
     dev = sats.device_satrec
     n, m = sats.n, t.size

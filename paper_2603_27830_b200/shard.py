@@ -65,7 +65,15 @@ def propagate_sharded(columns: np.ndarray, times, precision: int = 32, group=Non
     times = np.asarray(times)
     axis, lo, hi = shard_plan(columns.shape[1], times.shape[0], world, rank)
     if hi <= lo:
-        return None, (axis, lo, hi)
+        # an empty shard still takes part in collectives (gather_grid):
+        # zero-row (or zero-column) grids on this rank's device
+        from . import _device
+        from .batch import BatchResult
+        d = _device.require_cuda(device)
+        n, m = (0, times.shape[0]) if axis == "rows" else (columns.shape[1], 0)
+        planes = torch.empty((6, n, m), dtype=_device.torch_dtype(precision), device=d)
+        error = torch.empty((n, m), dtype=torch.int32, device=d)
+        return BatchResult(planes=planes, error=error, n=n, m=m), (axis, lo, hi)
     if axis == "rows":
         sats = init_batch(columns[:, lo:hi], precision=precision, device=device)
         return propagate_batch_device(sats, times), (axis, lo, hi)
@@ -78,8 +86,11 @@ def gather_grid(planes: torch.Tensor, error: torch.Tensor, n_total: int, group=N
     """Assemble the full (6, N, M) / (N, M) grid on rank ``dst`` from the
     per-rank shards: row shards (``axis="rows"``, bounds from shard_bounds
     over ``n_total``) or time-column shards (``axis="cols"``, bounds over
-    ``m_total``).  Returns the tensors on ``dst`` and None elsewhere.  Works
-    with gloo (CPU tensors) and NCCL."""
+    ``m_total``).  Returns the tensors on ``dst`` and None elsewhere.  Every
+    rank must call it (empty shards pass zero-row tensors).  One
+    ``dist.gather`` per plane set: gloo on CPU tensors, NCCL on device
+    tensors (point-to-point under the hood), so only ``dst`` holds the
+    world's shards."""
     world, rank = world_info(group)
     if world == 1:
         return planes, error
@@ -96,26 +107,18 @@ def gather_grid(planes: torch.Tensor, error: torch.Tensor, n_total: int, group=N
     dev = planes.device
 
     def padded(x, shape):
+        if tuple(x.shape) == tuple(shape):
+            return x.contiguous()
         out = torch.zeros(shape, dtype=x.dtype, device=dev)
         out[tuple(slice(0, s) for s in x.shape)] = x
         return out
 
     p = padded(planes, (6, rows_max, m))
     e = padded(error, (rows_max, m))
-    if rank == dst:
-        plist = [torch.empty_like(p) for _ in range(world)]
-        elist = [torch.empty_like(e) for _ in range(world)]
-    else:
-        plist = elist = None
-    if dist.get_backend(group) == "nccl":
-        # NCCL has no gather; all_gather into every rank then keep dst's
-        plist = [torch.empty_like(p) for _ in range(world)]
-        elist = [torch.empty_like(e) for _ in range(world)]
-        dist.all_gather(plist, p, group=group)
-        dist.all_gather(elist, e, group=group)
-    else:
-        dist.gather(p, plist, dst=dst, group=group)
-        dist.gather(e, elist, dst=dst, group=group)
+    plist = [torch.empty_like(p) for _ in range(world)] if rank == dst else None
+    elist = [torch.empty_like(e) for _ in range(world)] if rank == dst else None
+    dist.gather(p, plist, dst=dst, group=group)
+    dist.gather(e, elist, dst=dst, group=group)
     if rank != dst:
         return None
     full_p = torch.cat([plist[r][:, :hi - lo] for r, (lo, hi) in enumerate(bounds)], dim=1)

@@ -814,3 +814,33 @@ def test_t_absmax_bound_only_changes_speed(corpus_columns):
         planes, codes = _alloc_grid(64, 129, 32, t_d.device)
         _device.propagate_grid(sats.device_satrec, t_d, planes, codes, t_absmax=bound)
         assert torch.equal(planes, ref.planes) and torch.equal(codes, ref.error)
+
+
+@pytest.mark.parametrize("precision,dtype", [(64, np.float64), (32, np.float32)])
+def test_hand_built_init_code_persists(real_elements, precision, dtype):
+    """A nonzero error_code_at_init of a hand-built SatInit persists in every
+    cell, whatever its value (kernel.py:529-534), e.g. 300 (beyond 8 bits)."""
+    import dataclasses as dc
+    pkg = _gpu()
+    init = pkg.sgp4_init(real_elements["ISS"], dtype=dtype)
+    edited = dc.replace(init, error_code_at_init=np.int32(300))
+    st = pkg.sgp4_propagate(edited, np.array([0.0, 60.0, 720.0], dtype=dtype))
+    assert st.error_code.tolist() == [300, 300, 300]
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_multi_device_path_bitwise(corpus_columns, precision, ndev):
+    """propagate_batch(devices=...) — satellite ranges on several GPUs of
+    one process, each D2H-ing into one pinned host grid — equals the
+    single-device grid bit for bit.  On a 1-GPU box the "devices" are the
+    same GPU named several times (separate streams, same code path)."""
+    import torch
+    pkg = _gpu()
+    sats = pkg.init_batch(corpus_columns[:, :257], precision=precision)
+    times = np.linspace(-60.0, 2880.0, 131)
+    single = pkg.propagate_batch(sats, times)
+    devs = [i % torch.cuda.device_count() for i in range(ndev)]
+    multi = pkg.propagate_batch(sats, times, devices=devs)
+    assert np.array_equal(multi.planes, single.planes, equal_nan=True)
+    assert np.array_equal(multi.error, single.error)

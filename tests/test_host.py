@@ -235,3 +235,16 @@ def test_scaling_sweep_validation():
         scaling_sweep("times", [4, 2], 10, [])
     with pytest.raises(ValueError):
         scaling_sweep("times", [2, 2], 10, [])
+
+
+def test_pack_rejects_init_codes_the_record_cannot_hold():
+    """A hand-built SatInit's error_code_at_init travels in the packed
+    record's 23-bit code field: codes outside [0, 2^23) are refused before
+    any GPU work instead of wrapping to a different (or zero) code."""
+    import pytest as _pytest
+    from paper_2603_27830_b200 import _device
+    from paper_2603_27830_b200.gravity import WGS72
+    sr = np.zeros((33, 2))
+    for bad in ([-1, 0], [0, 1 << 23]):
+        with _pytest.raises(ValueError, match="error_code_at_init"):
+            _device.pack_device(sr, np.array(bad), np.zeros(2, np.uint8), WGS72, 64)

@@ -110,3 +110,73 @@ def test_two_rank_gloo_time_shards_reassemble_bitwise(corpus_columns):
     ref_planes, ref_codes = oracle.grid(oracle.init_columns(cols, 64), times)
     assert np.array_equal(out["planes"], ref_planes)
     assert np.array_equal(out["codes"], ref_codes)
+
+
+def _empty_worker(rank, world, port, cols, times, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sgp4_oracle as oracle
+        n = cols.shape[1]
+        lo, hi = shard_bounds(n, world, rank)
+        if hi > lo:
+            planes, codes = oracle.grid(oracle.init_columns(cols[:, lo:hi], 64), times)
+            planes, codes = torch.from_numpy(planes), torch.from_numpy(codes)
+        else:                      # an empty shard still joins the collective
+            planes = torch.empty((6, 0, times.size), dtype=torch.float64)
+            codes = torch.empty((0, times.size), dtype=torch.int32)
+        got = gather_grid(planes, codes, n)
+        if rank == 0:
+            out["planes"] = got[0].numpy()
+            out["codes"] = got[1].numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_with_an_empty_shard(corpus_columns):
+    """One satellite, two ranks (rank 1's row shard is empty): every rank
+    joins the gather and rank 0 gets the full grid."""
+    from oracle import sgp4_oracle as oracle
+    cols = corpus_columns[:, :1]
+    times = np.linspace(0.0, 60.0, 1)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_empty_worker, args=(2, _free_port(), cols, times, out), nprocs=2, join=True)
+    ref_planes, ref_codes = oracle.grid(oracle.init_columns(cols, 64), times)
+    assert np.array_equal(out["planes"], ref_planes)
+    assert np.array_equal(out["codes"], ref_codes)
+
+
+def _gpu_worker(rank, world, port, cols, times, precision, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_27830_b200.shard import propagate_sharded
+        torch.cuda.set_device(0)
+        res, (axis, lo, hi) = propagate_sharded(cols, times, precision=precision, device="cuda:0")
+        got = gather_grid(res.planes.cpu(), res.error.cpu(), cols.shape[1], axis=axis,
+                          m_total=len(times))
+        if rank == 0:
+            out["planes"] = got[0].numpy()
+            out["codes"] = got[1].numpy()
+            out["axis"] = axis
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,precision", [(301, 77, 32), (301, 77, 64), (1, 1000, 32), (1, 1, 64)])
+def test_two_process_gpu_shards_bitwise_equal_single_launch(corpus_columns, n, m, precision):
+    """Two processes (one per shard) each run init + propagate on the GPU for
+    their satellite range (or time range, or an empty shard), the shards are
+    gathered, and the grid equals one single-process launch bit for bit."""
+    import paper_2603_27830_b200 as pkg
+    cols = np.tile(corpus_columns, (1, 1))[:, :n]
+    times = np.linspace(0.0, 1440.0, m)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_gpu_worker, args=(2, _free_port(), cols, times, precision, out), nprocs=2, join=True)
+    full = pkg.propagate_batch(pkg.init_batch(cols, precision=precision), times)
+    assert out["axis"] == ("cols" if n == 1 and m >= 2 else "rows")
+    assert np.array_equal(out["planes"], full.planes)
+    assert np.array_equal(out["codes"], full.error)
