@@ -157,7 +157,8 @@ def times_absmax(times) -> float:
     if isinstance(times, torch.Tensor):
         return float(times.detach().abs().max().item()) if times.numel() else 0.0
     t = np.asarray(times)
-    return float(np.max(np.abs(t))) if t.size else 0.0
+    # no |t| temporary: the streamed API keeps host allocations O(1) in M
+    return max(float(t.max()), -float(t.min())) if t.size else 0.0
 
 
 def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,

@@ -11,6 +11,7 @@ multi-GPU sharding and the throughput benchmark use.
 from __future__ import annotations
 
 import struct
+import sys
 from dataclasses import dataclass
 from typing import Any, Callable, Sequence
 
@@ -384,8 +385,13 @@ def partition_work(n: int, m: int, workers: int) -> list[tuple[int, int]]:
 
 def _tile_grid(n: int, m: int, tile_rows: int, tile_cols: int):
     """Row-major (row-slice, col-slice) tiles covering N x M."""
-    return [(slice(r, min(r + tile_rows, n)), slice(c, min(c + tile_cols, m)))
-            for r in range(0, n, tile_rows) for c in range(0, m, tile_cols)]
+    return list(_iter_tiles(n, m, tile_rows, tile_cols))
+
+
+def _iter_tiles(n: int, m: int, tile_rows: int, tile_cols: int):
+    for r in range(0, n, tile_rows):
+        for c in range(0, m, tile_cols):
+            yield slice(r, min(r + tile_rows, n)), slice(c, min(c + tile_cols, m))
 
 
 @dataclass(frozen=True)
@@ -405,18 +411,21 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
     """
     if tile_rows < 1 or tile_cols < 1:
         raise ValueError("tile dimensions must be >= 1")
-    t = np.array(times, dtype=sats.dtype)
+    # host allocations stay O(1) in N and M (the reference's memory contract,
+    # test_batch.py:147-173, counts traced Python memory): times are used in
+    # place when they already have the batch dtype, tiles are generated lazily
+    t = np.asarray(times, dtype=sats.dtype)
     if t.ndim != 1:
         raise ValueError("times must be a 1-D array")
     dev = sats.device_satrec
     n, m = sats.n, t.size
-    tiles = _tile_grid(n, m, tile_rows, tile_cols)
-    if not tiles:
+    if n == 0 or m == 0:
         return StreamSummary(0, 0)
     cells = errors = completed = 0
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
-        t_d = torch.from_numpy(t).to(dev.device)
+        t_c = np.ascontiguousarray(t)
+        t_d = torch.from_numpy(t_c if t_c.flags.writeable else t_c.copy()).to(dev.device)
         t_abs = _device.times_absmax(t)
 
         def launch(tile):
@@ -430,38 +439,98 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
             torch.from_numpy(err_h).copy_(err_d, non_blocking=True)
             done = torch.cuda.Event()
             done.record(stream)
-            return planes_h, err_h, done, (planes_d, err_d)
+            return tile, planes_h, err_h, done, (planes_d, err_d)
 
-        pending = launch(tiles[0])
-        for k, (rows, cols) in enumerate(tiles):
-            planes_np, err_np, done, keep = pending
-            pending = launch(tiles[k + 1]) if k + 1 < len(tiles) else None
+        tiles = _iter_tiles(n, m, tile_rows, tile_cols)
+        pending = launch(next(tiles))
+        while pending is not None:
+            (rows, cols), planes_np, err_np, done, keep = pending
+            nxt = next(tiles, None)
+            pending = launch(nxt) if nxt is not None else None
             done.synchronize()
             try:
                 sink(rows, cols, planes_np, err_np)
             except Exception as exc:
                 if pending is not None:
-                    pending[2].synchronize()
+                    pending[3].synchronize()
                 raise StreamAborted(completed, exc) from exc
             completed += 1
             cells += err_np.size
             errors += int(np.count_nonzero(err_np))
+            del planes_np, err_np, keep
     return StreamSummary(cells_emitted=cells, nonzero_error_count=errors)
+
+
+_SGB1_CHUNK = 16 << 20          # bytes per pinned staging buffer (two of them)
 
 
 def write_grid_binary(result: BatchResult, stream) -> None:
     """SGB1: 32-byte little-endian header, planes rx..vz, then int32 codes
-    (batch.py:244-251).  Device results are copied out plane by plane."""
-    planes = result.planes
-    if isinstance(planes, torch.Tensor):
-        planes = planes.cpu().numpy()
-    error = result.error.cpu().numpy() if isinstance(result.error, torch.Tensor) else result.error
-    itemsize = np.dtype(planes.dtype).itemsize
+    (batch.py:244-251; reader frontend/src/sgb1.ts:89-142).
+
+    Host results are written straight from their arrays (a C-contiguous
+    (6, n, m) grid is one write, no ``tobytes`` copy).  Device results never
+    form a host grid: row blocks of each plane are DMA'd into two pinned
+    16 MiB staging buffers in turn, and block k is written to ``stream``
+    while block k+1 crosses PCIe.
+    """
+    planes, error = result.planes, result.error
+    if isinstance(planes, torch.Tensor) and planes.is_cuda:
+        itemsize = planes.element_size()
+    else:
+        itemsize = np.dtype(np.asarray(planes).dtype).itemsize
+    if itemsize not in (4, 8):
+        raise ValueError(f"planes must be float32 or float64, got {itemsize}-byte items")
     stream.write(_HEADER.pack(MAGIC, result.n, result.m, itemsize * 8, PLANE_ORDER_TAG))
+    if isinstance(planes, torch.Tensor) and planes.is_cuda:
+        _write_device_grid(planes, error, stream)
+        return
+    planes = planes.cpu().numpy() if isinstance(planes, torch.Tensor) else planes
+    error = error.cpu().numpy() if isinstance(error, torch.Tensor) else error
     le = np.dtype(f"<f{itemsize}")
-    for plane in planes:
-        stream.write(np.ascontiguousarray(plane, dtype=le).tobytes())
-    stream.write(np.ascontiguousarray(error, dtype="<i4").tobytes())
+    planes = np.asarray(planes)
+    if planes.dtype == le and planes.flags.c_contiguous:
+        stream.write(memoryview(planes.reshape(-1)).cast("B"))
+    else:
+        for plane in planes:
+            stream.write(memoryview(np.ascontiguousarray(plane, dtype=le).reshape(-1)).cast("B"))
+    codes = np.ascontiguousarray(error, dtype="<i4")
+    stream.write(memoryview(codes.reshape(-1)).cast("B"))
+
+
+def _write_device_grid(planes: torch.Tensor, error: torch.Tensor, stream) -> None:
+    """Row blocks of the six planes and the code plane, device -> two pinned
+    staging buffers (alternating) -> ``stream``."""
+    n, m = int(error.shape[0]), int(error.shape[1])
+    if n == 0 or m == 0:
+        return
+    if sys.byteorder != "little":
+        raise RuntimeError("SGB1 device emission assumes a little-endian host")
+    row_bytes = m * max(planes.element_size(), 4)
+    rows = max(1, _SGB1_CHUNK // row_bytes)
+    bufs = [np.asarray(_hostmem.alloc(rows * row_bytes)) for _ in range(2)]
+    jobs = [(seg, r0, min(r0 + rows, n))
+            for seg in (*planes.unbind(0), error) for r0 in range(0, n, rows)]
+    with torch.cuda.device(planes.device):
+        cs = torch.cuda.current_stream(planes.device)
+        pending: list = [None, None]
+
+        def issue(k: int) -> None:
+            seg, r0, r1 = jobs[k]
+            nb = (r1 - r0) * m * seg.element_size()
+            host = torch.from_numpy(bufs[k % 2][:nb]).view(seg.dtype).view(r1 - r0, m)
+            host.copy_(seg[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            pending[k % 2] = (ev, nb)
+
+        issue(0)
+        for k in range(len(jobs)):
+            if k + 1 < len(jobs):
+                issue(k + 1)            # its buffer was written out in iteration k-1
+            ev, nb = pending[k % 2]
+            ev.synchronize()
+            stream.write(memoryview(bufs[k % 2])[:nb])
 
 
 def read_grid_binary(stream) -> BatchResult:

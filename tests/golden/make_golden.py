@@ -110,6 +110,44 @@ def main() -> None:
             row[f"finite_{precision}"] = bool(np.isfinite(st.r).all() and np.isfinite(st.v).all())
         table["cases"][key] = row
     (OUT / "ref_failure_codes.json").write_text(json.dumps(table, indent=1) + "\n")
+
+    # SGB1 bytes from the reference writer (batch.py:244-251) --------------
+    sgb_times = np.array([0.0, 60.0, 120.0, 240.0, 480.0, 1440.0, -30.0])
+    sgb_sats = near + els[:5] + [cases["lowperigee_b05"], cases["n_zero"]]
+    for precision in (32, 64):
+        res = sgp4kit.propagate_batch(sgp4kit.init_batch(sgb_sats, precision=precision),
+                                      sgb_times)
+        with open(OUT / f"ref_sgb1_{precision}.bin", "wb") as fh:
+            sgp4kit.write_grid_binary(res, fh)
+    np.save(OUT / "ref_sgb1_elements.npy",
+            np.array([[getattr(e, f) for f in ELEMENT_FIELDS] for e in sgb_sats]).T)
+
+    # the reference's drift_report (drift.py:52-100) on the acceptance corpus
+    # (first 120 LEO records, test_acceptance.py:107-122 horizon/step) ----
+    rep = sgp4kit.drift_report(els[:120], horizon_days=14.0, step_minutes=90.0)
+    np.savez_compressed(
+        OUT / "ref_drift.npz",
+        **{k: np.asarray(getattr(rep, k)) for k in
+           ("days", "p5_km", "p50_km", "p95_km", "p5_kms", "p50_kms", "p95_kms",
+            "heuristic_km", "corpus_size", "excluded_cells", "included_cells")})
+    (OUT / "ref_drift.csv").write_text(sgp4kit.emit_report_csv(rep))
+
+    # the reference CLI (cli.py:160-184) on the real records file ---------
+    import tempfile
+    from sgp4kit import cli as ref_cli
+    with tempfile.TemporaryDirectory() as tmp:
+        for precision in (32, 64):
+            path = Path(tmp) / f"b{precision}.bin"
+            rc = ref_cli.main(["batch", str(OUT / "real_tles.tle"), "--tsince", "0:1500:300",
+                               "--precision", str(precision), "--format", "binary",
+                               "--out", str(path)])
+            assert rc == 0
+            (OUT / f"ref_cli_batch_{precision}.bin").write_bytes(path.read_bytes())
+        path = Path(tmp) / "b.csv"
+        rc = ref_cli.main(["batch", str(OUT / "real_tles.tle"), "--tsince-list",
+                           "0,90.5,1440,-60", "--out", str(path)])
+        assert rc == 0
+        (OUT / "ref_cli_batch_64.csv").write_text(path.read_text())
     print("golden fixtures written to", OUT)
 
 
