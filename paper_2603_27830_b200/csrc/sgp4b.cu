@@ -52,6 +52,9 @@
 #ifndef SGP4B_K2_SERIES
 #define SGP4B_K2_SERIES 1           // class-2 (e < 0.1) series for 1/pl_lp, 1/den, 1/(1+betal)
 #endif
+#ifndef SGP4B_F64_DRAG32
+#define SGP4B_F64_DRAG32 1          // fp64 class-1 cell: drag trig/cubic on the SFU/FP32 pipes
+#endif
 #ifndef SGP4B_MINB64
 #define SGP4B_MINB64 1
 #endif
@@ -354,21 +357,37 @@ constexpr unsigned kHi2m10 = 0x3F500000u;    // 2^-10
 // significant bits, so k C1 is exact for |k| < 2^26, |x| < 8e5 rad), and the
 // quotient k comes from the 1.5 2^52 shifter, whose low word is the table
 // index.  TrigLib (libdevice) serves the init kernel.
-constexpr int kTabN = 512;
-constexpr double kTabScale = 81.487330863050417;       // 512 / (2 pi)
-constexpr double kTabC1 = 0.012271846295334399;         // 2 pi / 512 to 27 bits
-constexpr double kTabC2 = 7.750731091254222e-12;         // 2 pi / 512 - C1
+#ifndef SGP4B_TABN
+#define SGP4B_TABN 1024
+#endif
+constexpr int kTabN = SGP4B_TABN;
+constexpr double kTabScale = kTabN / 6.283185307179586476925286766559;   // N / (2 pi)
+// 2 pi / N rounded to 27 significant bits (k C1 exact for |k| < 2^26), and
+// the remainder
+constexpr double kTabStep = 6.283185307179586476925286766559 / kTabN;
+constexpr double kTabC1Scale = kTabN <= 512 ? 17179869184.0 * 2.0 : 17179869184.0 * (kTabN / 1024);
+constexpr double kTabC1 = (double)(long long)(kTabStep * kTabC1Scale) / kTabC1Scale;
+// (2 pi = fl(2 pi) + 2.4492935982947064e-16: the low word keeps k C2 exact
+// to ~1e-21 for the |k| < 2^26 the reduction admits)
+constexpr double kTabC2 = (6.283185307179586476925286766559 - kTabC1 * kTabN) / kTabN +
+                          2.4492935982947064e-16 / kTabN;
+// with |r| <= pi / N the sine needs r^5/120 only for N < 1024 (at N = 1024
+// it is below 2.3e-15, so every evaluation takes the short form)
+constexpr bool kTabShortSin = kTabN >= 1024;
 constexpr double kShift52 = 6755399441055744.0;         // 1.5 * 2^52
 // fp64 constants whose low words are nonzero live in constant memory, so
 // DFMA reads them as c[][] operands instead of rematerialising 64-bit
 // immediates into register pairs every cell
-__constant__ double c_k64[6] = {kTabScale, kTabC1, kTabC2, 1.0 / 120.0, -1.0 / 6.0, 1.0 / 24.0};
+__constant__ double c_k64[8] = {kTabScale, kTabC1, kTabC2, 1.0 / 120.0, -1.0 / 6.0, 1.0 / 24.0,
+                                kInvTwoPi, kTwoPi};
 #define K_TABSCALE c_k64[0]
 #define K_TABC1 c_k64[1]
 #define K_TABC2 c_k64[2]
 #define K_1_120 c_k64[3]
 #define K_M1_6 c_k64[4]
 #define K_1_24 c_k64[5]
+#define K_INV2PI c_k64[6]
+#define K_2PI c_k64[7]
 
 struct TrigTab {
   const double2* tab;
@@ -379,7 +398,7 @@ struct TrigTab {
     double r = fma(-k, K_TABC1, x);
     r = fma(-k, K_TABC2, r);
     const double z = r * r;
-    const double sr = fma(r * z, fma(z, K_1_120, K_M1_6), r);
+    const double sr = kTabShortSin ? fma(r * z, K_M1_6, r) : fma(r * z, fma(z, K_1_120, K_M1_6), r);
     const double cr = fma(z, fma(z, K_1_24, -0.5), 1.0);
     const double2 e = tab[idx];                          // (sin a, cos a)
     s = fma(e.x, cr, e.y * sr);
@@ -684,6 +703,7 @@ __device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long
     em = fma(-R[Q_BC4], t, R[Q_E0]);
     argpm = argpdf;
   } else {
+#if !SGP4B_F64_DRAG32
     const double xmdf = fma(R[Q_MDOT], t, R[Q_MO]);
     double sx, cx;
     tr.short_sin(xmdf, sx, cx);
@@ -695,6 +715,27 @@ __device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long
     const double tt = temp * temp;
     const double smm = fma(sx, fma(tt, -0.5, 1.0), (cx * temp) * fma(tt, K_M1_6, 1.0));
     em = fma(-R[Q_BC5], smm, fma(-R[Q_BC4], t, R[Q_E0]));
+#else
+    // drag, off the FP64 pipe: xmdf only reaches the state through the drag
+    // cubic (coefficients A1..A3, times em when it moves argpm) and through
+    // bstar cc5 sin(mm) (< 4e-6), so after an fp64 reduction to [-pi, pi]
+    // its sin/cos come from the SFU and the cubic and sin(mm) are fp32: the
+    // position error this adds is below 1e-8 km (2 coef bstar 4e-7 a), and
+    // the conversions ride the idle XU
+    const double xmdf = fma(R[Q_MDOT], t, R[Q_MO]);
+    const double kx = fma(xmdf, K_INV2PI, kShift52) - kShift52;
+    float sx, cx;
+    __sincosf((float)fma(-kx, K_2PI, xmdf), &sx, &cx);
+    const float cub = cx * fmaf(fmaf(cx, (float)R[Q_A3], (float)R[Q_A2]), cx, (float)R[Q_A1]);
+    const double temp = fma(R[Q_OMGCOF], t, R[Q_A0]) + (double)cub;
+    argpm = argpdf - temp;
+    sqam = fma(t, fma(t, fma(t, fma(t, R[Q_SD4], R[Q_SD3]), R[Q_SD2]), R[Q_SC1]), R[Q_S]);
+    nol = t2 * fma(t, fma(t, fma(t, R[Q_N5], R[Q_N4]), R[Q_N3]), R[Q_N2]);
+    const float tf = (float)temp;
+    const float tt = tf * tf;
+    const float smm = fmaf(sx, fmaf(tt, -0.5f, 1.0f), (cx * tf) * fmaf(tt, -1.0f / 6.0f, 1.0f));
+    em = fma(-R[Q_BC4], t, R[Q_E0]) - (double)((float)R[Q_BC5] * smm);
+#endif
     ok = small_abs(temp, kHi2m6);
   }
   const double asq = __longlong_as_double(dbits(sqam) & 0x7fffffffffffffffLL);   // |sqam|
@@ -1219,7 +1260,10 @@ __device__ __forceinline__ int record_flags(const double* f, int init_code, bool
 }
 
 // fp64 record values (flags slot left 0; see record_flags)
-__device__ __forceinline__ void record_values(const double* f, const Grav& g, double* out) {
+// ao_sc = (ao, sin inclo, cos inclo) when the caller already has them (the
+// init kernel); otherwise they are recomputed from the satrec fields
+__device__ __forceinline__ void record_values(const double* f, const Grav& g, double* out,
+                                              const double* ao_sc = nullptr) {
   const double no = f[F_NO_UNKOZAI];
   const bool bad_nm = no <= 0.0;
   const double nm_safe = bad_nm ? 1.0e-4 : no;
@@ -1246,11 +1290,17 @@ __device__ __forceinline__ void record_values(const double* f, const Grav& g, do
   out[S_T4COF] = f[F_T4COF];
   out[S_T5COF] = f[F_T5COF];
   out[S_NO] = no;
-  out[S_AM0] = pow2o3(g.xke / nm_safe);
+  // (xke / nm_safe)^(2/3) is the init's ao unless n <= 0
+  out[S_AM0] = (ao_sc != nullptr && !bad_nm) ? ao_sc[0] : pow2o3(g.xke / nm_safe);
   out[S_ECCO] = f[F_ECCO];
   out[S_INCLO] = f[F_INCLO];
   double si, ci;
-  sincos(f[F_INCLO], &si, &ci);
+  if (ao_sc != nullptr) {
+    si = ao_sc[1];
+    ci = ao_sc[2];
+  } else {
+    sincos(f[F_INCLO], &si, &ci);
+  }
   out[S_SINIO] = si;
   out[S_COSIO] = ci;
   out[S_AYCOF] = f[F_AYCOF];
@@ -1390,6 +1440,69 @@ __device__ __forceinline__ void store_record<float>(const double* f, const doubl
 // ======================================================================
 // Init (kernel.py:154-322), fp64, one thread per satellite
 // ======================================================================
+
+// The epoch evaluation of kernel.py:316-322: _propagate at t = 0, where the
+// secular and drag terms vanish exactly (xmdf = mo, tempa = 1, tempe =
+// templ = delm = 0, so mm = mo, argpm = argpo, nodem = nodeo, em = ecco,
+// am = ao), reduced to what decides its code: _first_error 2 > 1 > 4 > 6
+// (kernel.py:393-414, 419-431, 325-349, 440-469, 495-502) in the
+// reference's operation order, with the reference Kepler loop.  Only the
+// code is kept, so the orientation and velocity terms are not formed.
+__device__ int epoch_code(const double* f, double ao, const Grav& g) {
+  const double tiny = DBL_MIN;
+  const bool bad_nm = f[F_NO_UNKOZAI] <= 0.0;
+  const double am = bad_nm ? pow2o3(g.xke / 1.0e-4) : ao;        // tempa = 1
+  const double am_safe = gmax(am, tiny);
+  double em = f[F_ECCO];
+  const bool bad_em = (em >= 1.0) || (em < -0.001);
+  em = em < 1.0e-6 ? 1.0e-6 : em;
+  // floor-mods as kernel.py:407-411 (templ = 0: mm = mo)
+  const double nodeo = f[F_NODEO];
+  const double nodem = nodeo >= 0.0 ? pymod_2pi(nodeo) : -pymod_2pi(-nodeo);
+  const double argpm = pymod_2pi(f[F_ARGPO]);
+  const double xlm = pymod_2pi(f[F_MO] + f[F_ARGPO] + nodeo);
+  const double mm = pymod_2pi(xlm - argpm - nodem);
+  double sa, ca;
+  sincos(argpm, &sa, &ca);
+  const double axnl = em * ca;
+  const double temp_lp = 1.0 / gmax(am_safe * (1.0 - em * em), tiny);
+  const double aynl = em * sa + temp_lp * f[F_AYCOF];
+  const double xl = mm + argpm + nodem + temp_lp * f[F_XLCOF] * axnl;
+  const double u = pymod_2pi(xl - nodem);
+  // solve_kepler  kernel.py:325-349
+  double eo1 = u;
+  bool live = true;
+  for (int it = 0; it < 10 && live; ++it) {
+    double s, c;
+    sincos(eo1, &s, &c);
+    double step = 1.0 - c * axnl - s * aynl;
+    step = (u - aynl * c + axnl * s - eo1) / step;
+    step = step >= 0.95 ? 0.95 : (step <= -0.95 ? -0.95 : step);
+    eo1 += step;
+    live = fabs(step) >= 1.0e-12;
+  }
+  double sineo1, coseo1;
+  sincos(eo1, &sineo1, &coseo1);
+  const double ecose = axnl * coseo1 + aynl * sineo1;
+  const double esine = axnl * sineo1 - aynl * coseo1;
+  const double el2 = axnl * axnl + aynl * aynl;
+  const double pl = am_safe * (1.0 - el2);
+  const bool bad_pl = pl < 0.0;
+  const double pl_safe = gmax(pl, tiny);
+  const double rl = am_safe * (1.0 - ecose);
+  const double rl_safe = rl == 0.0 ? tiny : rl;
+  const double betal = sqrt(gmax(1.0 - el2, tiny));
+  const double temp = esine / (1.0 + betal);
+  const double sinu = am_safe / rl_safe * (sineo1 - aynl - axnl * temp);
+  const double cos2u = 1.0 - 2.0 * sinu * sinu;
+  const double ipl = 1.0 / pl_safe;
+  const double temp1 = 0.5 * g.j2 * ipl;
+  const double temp2 = temp1 * ipl;
+  const double mrt = rl * (1.0 - 1.5 * temp2 * betal * f[F_CON41]) +
+                     0.5 * temp1 * f[F_X1MTH2] * cos2u;
+  return bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : (mrt < 1.0) ? 6 : 0;
+}
+
 __device__ void init_one(const double el[7], const Grav& g, double* f, double* v, int& code,
                          bool& isimp_out) {
   const double tiny = DBL_MIN;
@@ -1404,7 +1517,8 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const double eccsq = ecco * ecco;
   const double omeosq = gmax(1.0 - eccsq, tiny);
   const double rteosq = sqrt(omeosq);
-  const double cosio = cos(inclo);
+  double sinio, cosio;
+  sincos(inclo, &sinio, &cosio);
   const double cosio2 = cosio * cosio;
 
   // un-Kozai  :187-193
@@ -1417,7 +1531,6 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const bool deep_space = kTwoPi / no_unkozai >= 225.0;             // :195
 
   const double ao = pow2o3(xke / no_unkozai);
-  const double sinio = sin(inclo);
   const double po = ao * omeosq;
   const double con42 = 1.0 - 5.0 * cosio2;
   const double con41 = -con42 - cosio2 - cosio2;
@@ -1458,11 +1571,14 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const double cc3 = ecc_small ? 0.0 * ecco
                                : -2.0 * coef * tsi * j3oj2 * no_unkozai * sinio / ecco_guard;
   const double x1mth2 = 1.0 - cosio2;
+  double sinargp, cosargp;
+  sincos(argpo, &sinargp, &cosargp);
   const double cc4 = 2.0 * no_unkozai * coef1 * ao * omeosq *
       (eta * (2.0 + 0.5 * etasq) + ecco * (0.5 + 2.0 * etasq) -
        j2 * tsi / (ao * psisq) *
            (-3.0 * con41 * (1.0 - 2.0 * eeta + etasq * (1.5 - 0.5 * eeta)) +
-            0.75 * x1mth2 * (2.0 * etasq - eeta * (1.0 + etasq)) * cos(2.0 * argpo)));
+            0.75 * x1mth2 * (2.0 * etasq - eeta * (1.0 + etasq)) *
+                (cosargp - sinargp) * (cosargp + sinargp)));     // cos(2 argpo)
   const double cc5 = 2.0 * coef1 * ao * omeosq * (1.0 + 2.75 * (etasq + eeta) + eeta * etasq);
   const double cosio4 = cosio2 * cosio2;
   const double temp1 = 1.5 * j2 * pinvsq * no_unkozai;
@@ -1476,7 +1592,7 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const double xhdot1 = -temp1 * cosio;
   const double nodedot = xhdot1 + (0.5 * temp2 * (4.0 - 19.0 * cosio2) +
                                    2.0 * temp3 * (3.0 - 7.0 * cosio2)) * cosio;
-  const double omgcof = bstar * cc3 * cos(argpo);
+  const double omgcof = bstar * cc3 * cosargp;
   const double eeta_guard = fabs(eeta) < tiny ? tiny : eeta;
   const double xmcof = ecc_small ? 0.0 * ecco : -kX2o3 * coef * bstar / eeta_guard;
   const double nodecf = 3.5 * omeosq * xhdot1 * cc1;
@@ -1484,9 +1600,10 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const double xlcof_den = fabs(cosio + 1.0) > 1.5e-12 ? 1.0 + cosio : 1.5e-12;
   const double xlcof = -0.25 * j3oj2 * sinio * (3.0 + 5.0 * cosio) / xlcof_den;
   const double aycof = -0.5 * j3oj2 * sinio;
-  const double delmotemp = 1.0 + eta * cos(mo);
+  double sinmao, cosmo;
+  sincos(mo, &sinmao, &cosmo);
+  const double delmotemp = 1.0 + eta * cosmo;
   const double delmo = delmotemp * delmotemp * delmotemp;
-  const double sinmao = sin(mo);
   const double x7thm1 = 7.0 * cosio2 - 1.0;
 
   // higher-order drag, zero in simplified mode  :278-294
@@ -1517,40 +1634,64 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   code = bad_n ? 2 : bad_e ? 1 : deep_space ? 7 : 0;
   isimp_out = isimp;
 
-  // epoch evaluation  :316-322 (the general cell on an fp64 record built
-  // with no persistent code)
-  record_values(f, g, v);
-  double rec[S_COUNT];
-  store_record<double>(f, v, record_flags(f, 0, isimp), isimp, g, rec);
-  RecS<double> R;
-  R.p = rec;
-  Cell64 c0;
-  cell64_general(R, 0.0, g.re, g.vkm, TrigLib{}, c0);
-  if (code == 0) code = c0.code;
+  // record values for the propagate kernels, reusing ao and sin/cos inclo
+  const double ao_sc[3] = {ao, sinio, cosio};
+  record_values(f, g, v, ao_sc);
+  // epoch evaluation  :316-322
+  if (code == 0) code = epoch_code(f, ao, g);
 }
 
-__global__ void init_kernel(const double* __restrict__ el, int64_t n, Grav g,
-                            double* __restrict__ satrec, int32_t* __restrict__ codes,
-                            uint8_t* __restrict__ isimp, void* __restrict__ rec, int precision) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double e[7];
-#pragma unroll
-  for (int k = 0; k < 7; ++k) e[k] = el[k * n + i];
+// One warp per block (the fp64 chains are long and latency-bound: spreading
+// satellites over every SM shortens the kernel).  The packed records (AoS,
+// 160/320 B per satellite) are staged in shared memory (odd stride: no bank
+// conflicts) and written by the warp as consecutive words, i.e. coalesced,
+// instead of 40 stores per lane strided by a whole record.
+constexpr int kStageStride = S_COUNT + 1;
+
+template <typename T>
+__device__ __forceinline__ void write_records(const double* f, const double* v, int flags,
+                                              bool simp, const Grav& g, bool valid,
+                                              int64_t i0, int64_t n, T* __restrict__ rec,
+                                              unsigned char* stage) {
+  const int lane = threadIdx.x & 31;
+  T* st = reinterpret_cast<T*>(stage);
+  if (valid) store_record<T>(f, v, flags, simp, g, st + lane * kStageStride);
+  __syncwarp();
+  T* dst = rec + i0 * S_COUNT;
+  const int words = (int)(min((int64_t)32, n - i0) * S_COUNT);
+  for (int k = lane; k < words; k += 32) {
+    const int r = k / S_COUNT;
+    dst[k] = st[r * kStageStride + (k - r * S_COUNT)];
+  }
+}
+
+__global__ void __launch_bounds__(32) init_kernel(
+    const double* __restrict__ el, int64_t n, Grav g, double* __restrict__ satrec,
+    int32_t* __restrict__ codes, uint8_t* __restrict__ isimp, void* __restrict__ rec,
+    int precision) {
+  __shared__ __align__(16) unsigned char stage[32 * kStageStride * sizeof(double)];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int64_t i = i0 + threadIdx.x;
+  const bool valid = i < n;
   double f[F_COUNT], v[S_COUNT];
-  int code;
-  bool simp;
-  init_one(e, g, f, v, code, simp);
+  int code = 0;
+  bool simp = false;
+  if (valid) {
+    double e[7];
 #pragma unroll
-  for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
-  codes[i] = code;
-  isimp[i] = simp ? 1 : 0;
+    for (int k = 0; k < 7; ++k) e[k] = el[k * n + i];
+    init_one(e, g, f, v, code, simp);
+#pragma unroll
+    for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
+    codes[i] = code;
+    isimp[i] = simp ? 1 : 0;
+  }
   if (rec != nullptr) {
-    const int flags = record_flags(f, code, simp);
+    const int flags = valid ? record_flags(f, code, simp) : 0;
     if (precision == 64)
-      store_record<double>(f, v, flags, simp, g, static_cast<double*>(rec) + i * S_COUNT);
+      write_records<double>(f, v, flags, simp, g, valid, i0, n, static_cast<double*>(rec), stage);
     else
-      store_record<float>(f, v, flags, simp, g, static_cast<float*>(rec) + i * S_COUNT);
+      write_records<float>(f, v, flags, simp, g, valid, i0, n, static_cast<float*>(rec), stage);
   }
 }
 
