@@ -112,6 +112,14 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
                       int64_t n, int64_t m, double* dr_dev, double* dv_dev,
                       void* stream);
 
+/* Row summary of a code plane: flags_dev[i] = 1 when row i (codes_dev +
+ * i*code_stride, m entries) holds a nonzero code, else 0.  Lets the host
+ * copy of a BatchResult (batch.py:177-183, the int32 error plane) move only
+ * the rows that carry codes over PCIe and zero-fill the others in host
+ * memory, since most catalogues have no failing cells. */
+int sgp4b_code_rows(const int32_t* codes_dev, int64_t n, int64_t m,
+                    int64_t code_stride, uint8_t* flags_dev, void* stream);
+
 /* Newton solve of SGP4's Kepler equation, elementwise (kernel.py:325-349). */
 int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev,
                        const void* u_dev, int64_t n, int precision,

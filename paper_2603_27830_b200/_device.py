@@ -207,3 +207,15 @@ def solve_kepler_device(axnl: torch.Tensor, aynl: torch.Tensor, u: torch.Tensor,
         axnl.data_ptr(), aynl.data_ptr(), u.data_ptr(), int(u.numel()), precision,
         out.data_ptr(), _stream(u.device)))
     return out
+
+
+def code_rows(codes: torch.Tensor, flags: torch.Tensor) -> None:
+    """flags[i] (uint8) = 1 when row i of the (n, m) int32 code plane holds
+    a nonzero code (``sgp4b_code_rows``)."""
+    n, m = int(codes.shape[0]), int(codes.shape[1])
+    if codes.dtype != torch.int32 or codes.stride(1) != 1:
+        raise ValueError("codes must be an int32 (n, m) plane with contiguous columns")
+    if flags.dtype != torch.uint8 or flags.numel() < n or flags.device != codes.device:
+        raise ValueError("flags must be a uint8 tensor of n entries on the codes' device")
+    _native.check(_native.load().sgp4b_code_rows(
+        codes.data_ptr(), n, m, codes.stride(0), flags.data_ptr(), _stream(codes.device)))

@@ -68,7 +68,9 @@ class PinnedBlock:
 
     def __del__(self):
         if self.ptr:
-            _released.append((self.size, self.ptr))
+            q = _released
+            if q is not None:               # None at interpreter teardown
+                q.append((self.size, self.ptr))
             self.ptr = 0
 
 
@@ -142,6 +144,33 @@ def empty(shapes_dtypes) -> list[np.ndarray]:
         nb = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
         out.append(raw[off:off + nb].view(dtype).reshape(shape))
     return out
+
+
+_ZERO_CHUNK = 4 << 20
+_fill_pool = None
+
+
+def _pool():
+    global _fill_pool
+    if _fill_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _fill_pool = ThreadPoolExecutor(max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)),
+                                        thread_name_prefix="sgp4b-zero")
+    return _fill_pool
+
+
+def zero_fill_async(arr: np.ndarray, lo: int, hi: int) -> list:
+    """Zero rows lo..hi of a C-contiguous array in ``_ZERO_CHUNK`` pieces on
+    a small thread pool (``ctypes.memset`` releases the GIL, so the fill runs
+    while the caller waits on a DMA).  Returns the futures."""
+    if hi <= lo:
+        return []
+    row = arr.strides[0]
+    base = arr.ctypes.data + lo * row
+    total = (hi - lo) * row
+    pool = _pool()
+    return [pool.submit(ctypes.memset, base + off, 0, min(_ZERO_CHUNK, total - off))
+            for off in range(0, total, _ZERO_CHUNK)]
 
 
 def empty_cache() -> None:

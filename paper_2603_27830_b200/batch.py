@@ -303,7 +303,7 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
     dev = sats.device_satrec
     n, m = sats.n, t.size
     devs = _devices(devices)
-    planes_h, error_h = _host_grid(n, m, dev.precision)
+    planes_h, error_h, flags_h = _host_grid(n, m, dev.precision)
     t_abs = _device.times_absmax(t)
     src_stream = torch.cuda.current_stream(dev.device)
     ready = torch.cuda.Event()
@@ -322,12 +322,16 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
                 t_d = torch.from_numpy(t).to(d, non_blocking=True)
                 planes, error = _alloc_grid(hi - lo, m, dev.precision, d)
                 _device.propagate_grid(sub, t_d, planes, error, t_absmax=t_abs)
+                codes = _CodesToHost(error, error_h[lo:hi], flags_h[lo:hi], stream)
                 for p in range(6):
                     torch.from_numpy(planes_h[p, lo:hi]).copy_(planes[p], non_blocking=True)
-                torch.from_numpy(error_h[lo:hi]).copy_(error, non_blocking=True)
-            jobs.append((stream, sub, t_d, planes, error))
-    for stream, *_ in jobs:
+            jobs.append((stream, codes, sub, t_d, planes, error))
+    for stream, codes, *_ in jobs:
+        with torch.cuda.stream(stream):
+            codes.finish()
+    for stream, codes, *_ in jobs:
         stream.synchronize()
+        codes.join()
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
 
 
@@ -349,21 +353,88 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None,
     t = _times(sats, times)
     dev = sats.device_satrec
     n, m = sats.n, t.size
-    planes_h, error_h = _host_grid(n, m, dev.precision)
+    planes_h, error_h, flags_h = _host_grid(n, m, dev.precision)
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
         t_d = torch.from_numpy(t).to(dev.device, non_blocking=True)
         res = propagate_batch_device(sats, t_d, t_absmax=_device.times_absmax(t))
+        codes = _CodesToHost(res.error, error_h, flags_h, stream)
         torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
-        torch.from_numpy(error_h).copy_(res.error, non_blocking=True)
+        codes.finish()
         stream.synchronize()
+        codes.join()
+    _last_transfer.update(d2h_bytes=planes_h.nbytes + codes.d2h_bytes,
+                          code_bytes_zero_filled=error_h.nbytes - (codes.d2h_bytes - flags_h.nbytes))
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
 
 
+_last_transfer: dict = {}
+
+
+def last_transfer() -> dict:
+    """Device->host bytes the last single-device ``propagate_batch`` moved
+    (planes + code-row flags + flagged code rows) and the code-plane bytes it
+    zero-filled on the host instead."""
+    return dict(_last_transfer)
+
+
+class _CodesToHost:
+    """D2H of an (n, m) int32 code plane that moves only the rows holding a
+    nonzero code.  ``__init__`` (before the planes' D2H is queued) runs
+    ``sgp4b_code_rows`` and copies the n row flags; ``finish`` waits for the
+    flags (they land a few µs after the grid kernel, while the planes are
+    still crossing PCIe), queues one D2H per run of flagged rows and
+    zero-fills every other row in host memory on a thread pool; ``join``
+    waits for the fills.  Every element of the host plane is written before
+    the caller returns; with many scattered flagged rows the whole plane is
+    copied instead."""
+
+    MAX_RUNS = 64
+
+    def __init__(self, error_d: torch.Tensor, error_h: np.ndarray, flags_h: np.ndarray, stream):
+        self.error_d, self.error_h, self.flags_h, self.stream = error_d, error_h, flags_h, stream
+        self.fills = []
+        n = error_d.shape[0]
+        flags_d = torch.empty(n, dtype=torch.uint8, device=error_d.device)
+        _device.code_rows(error_d, flags_d)
+        torch.from_numpy(flags_h).copy_(flags_d, non_blocking=True)
+        self.ready = torch.cuda.Event()
+        self.ready.record(stream)
+        self._keep = flags_d
+
+    def finish(self) -> None:
+        self.ready.synchronize()
+        n = self.error_h.shape[0]
+        rows = np.flatnonzero(self.flags_h)
+        runs = []
+        if rows.size:
+            cut = np.flatnonzero(np.diff(rows) != 1) + 1
+            starts = rows[np.r_[0, cut]]
+            ends = rows[np.r_[cut - 1, rows.size - 1]] + 1
+            runs = list(zip(starts.tolist(), ends.tolist()))
+        if len(runs) > self.MAX_RUNS or rows.size * 2 > n:
+            runs = [(0, n)]
+        row_bytes = self.error_h.strides[0]
+        self.d2h_bytes = self.flags_h.nbytes + sum(b - a for a, b in runs) * row_bytes
+        lo = 0
+        for a, b in runs:
+            torch.from_numpy(self.error_h[a:b]).copy_(self.error_d[a:b], non_blocking=True)
+            self.fills += _hostmem.zero_fill_async(self.error_h, lo, a)
+            lo = b
+        self.fills += _hostmem.zero_fill_async(self.error_h, lo, n)
+
+    def join(self) -> None:
+        for f in self.fills:
+            f.result()
+        self.fills = []
+
+
 def _host_grid(n: int, m: int, precision: int):
-    """(6, n, m) planes + (n, m) int32 codes in one pinned host block."""
+    """(6, n, m) planes + (n, m) int32 codes + (n,) uint8 code-row flags in
+    one pinned host block."""
     try:
-        return _hostmem.empty([((6, n, m), _device.np_dtype(precision)), ((n, m), np.int32)])
+        return _hostmem.empty([((6, n, m), _device.np_dtype(precision)), ((n, m), np.int32),
+                               ((n,), np.uint8)])
     except MemoryError:
         itemsize = 4 if precision == 32 else 8
         raise GridAllocationError(n, m, 6 * n * m * itemsize + 4 * n * m) from None
@@ -434,7 +505,7 @@ def propagate_batch_streamed(sats: SatBatch, times, tile_rows: int, tile_cols: i
             planes_d, err_d = _alloc_grid(tr, tc, dev.precision, dev.device)
             _device.propagate_grid(dev, t_d[cols].clone(), planes_d, err_d,
                                    rows=(rows.start, rows.stop), t_absmax=t_abs)
-            planes_h, err_h = _host_grid(tr, tc, dev.precision)
+            planes_h, err_h, _ = _host_grid(tr, tc, dev.precision)
             torch.from_numpy(planes_h).copy_(planes_d, non_blocking=True)
             torch.from_numpy(err_h).copy_(err_d, non_blocking=True)
             done = torch.cuda.Event()

@@ -33,6 +33,7 @@
 #include <stdarg.h>
 #include <math_constants.h>
 #include <type_traits>
+#include <algorithm>
 
 #include "../../include/sgp4b.h"
 
@@ -2242,6 +2243,34 @@ __global__ void drift_norms_kernel(const float* __restrict__ p32, const double* 
   dv[i] = sqrt(v2);
 }
 
+// flags[i] = 1 if row i of the code plane holds a nonzero code, else 0:
+// one warp per row (grid-stride), 16-byte loads when the rows are aligned.
+// Lets a host copy move only the rows that carry codes (most catalogues
+// have none) and zero-fill the rest itself.
+__global__ void __launch_bounds__(256) code_rows_kernel(const int32_t* __restrict__ codes,
+                                                        int64_t n, int64_t m, int64_t stride,
+                                                        uint8_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool vec = (stride % 4 == 0) && ((uintptr_t)codes % 16 == 0);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int32_t* row = codes + r * stride;
+    int any = 0;
+    int64_t j = 0;
+    if (vec) {
+      const int64_t m4 = m & ~(int64_t)3;
+      for (j = (int64_t)lane * 4; j < m4; j += 128) {
+        const int4 q = __ldcs(reinterpret_cast<const int4*>(row + j));
+        any |= q.x | q.y | q.z | q.w;
+      }
+      j = m4;
+    }
+    for (int64_t k = j + lane; k < m; k += 32) any |= __ldcs(row + k);
+    any = __any_sync(0xffffffffu, any != 0);
+    if (lane == 0) flags[r] = any ? 1 : 0;
+  }
+}
+
 bool grav_from(const double* grav, Grav& g) {
   if (grav == nullptr) return false;
   g.mu = grav[0]; g.re = grav[1]; g.xke = grav[2]; g.tumin = grav[3];
@@ -2324,7 +2353,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 3; }
+int sgp4b_abi_version(void) { return 4; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -2415,6 +2444,17 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
   drift_norms_kernel<<<blocks_for(cells, 256), 256, 0, (cudaStream_t)stream>>>(
       planes32_dev, planes64_dev, codes32_dev, codes64_dev, cells, dr_dev, dv_dev);
   return check_launch("sgp4b_drift_norms");
+}
+
+int sgp4b_code_rows(const int32_t* codes_dev, int64_t n, int64_t m, int64_t code_stride,
+                    uint8_t* flags_dev, void* stream) {
+  if (n <= 0 || m <= 0) return fail(SGP4B_EINVAL, "sgp4b_code_rows: empty grid");
+  if (!codes_dev || !flags_dev) return fail(SGP4B_EINVAL, "sgp4b_code_rows: null pointer argument");
+  if (code_stride < m) return fail(SGP4B_EINVAL, "sgp4b_code_rows: code_stride < m");
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 8);
+  code_rows_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(codes_dev, n, m,
+                                                                     code_stride, flags_dev);
+  return check_launch("sgp4b_code_rows");
 }
 
 int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev, const void* u_dev, int64_t n,

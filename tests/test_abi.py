@@ -60,6 +60,9 @@ GRAV = np.zeros(8)
     lambda L: L.sgp4b_propagate_grid(1, 4, 1, None, 8, 1.0, 32, GRAV.ctypes.data, 1, 8, 4, 1, 8, None),
     lambda L: L.sgp4b_propagate_pairs(1, 1, 1, None, 0, 1.0, 64, GRAV.ctypes.data, 1, 1, None),
     lambda L: L.sgp4b_solve_kepler(1, 1, 1, 4, 8, 1, None),
+    lambda L: L.sgp4b_code_rows(1, 0, 4, 4, 1, None),                           # n = 0
+    lambda L: L.sgp4b_code_rows(1, 4, 8, 4, 1, None),                           # stride < m
+    lambda L: L.sgp4b_code_rows(None, 4, 4, 4, 1, None),                        # null
 ])
 def test_invalid_arguments_rejected(call):
     lib = _native.load()

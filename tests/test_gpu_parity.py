@@ -562,6 +562,7 @@ def test_pinned_results_released(corpus_columns):
     import gc
     from paper_2603_27830_b200 import _hostmem
     pkg = _gpu()
+    gc.collect()                  # earlier tests' blocks still waiting in cycles
     _hostmem.empty_cache()
     base = _hostmem.stats()["pinned_bytes"]
     sats = pkg.init_batch(np.tile(corpus_columns, (1, 3))[:, :3000], precision=32)
@@ -720,6 +721,51 @@ def test_sparse_code_rows_with_errors(failure_table, corpus_columns, precision):
     summary = pkg.propagate_batch_streamed(sats, times, 3, 4, sink)
     assert np.array_equal(got, host.error)
     assert summary.nonzero_error_count == int(np.count_nonzero(host.error))
+
+
+def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
+    """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
+    unaligned row strides); propagate_batch zero-fills unflagged rows even
+    when its pinned block is reused from a call that left codes in it, and
+    copies the whole plane when the flagged rows are scattered."""
+    import torch
+    pkg = _gpu()
+    from paper_2603_27830_b200 import _device, _hostmem
+    rng = np.random.default_rng(7)
+    for n, m, ld in [(37, 130, 130), (37, 130, 133), (5, 3, 3), (300, 1000, 1000)]:
+        full = torch.zeros((n, ld), dtype=torch.int32, device="cuda")
+        rows = rng.choice(n, size=max(1, n // 5), replace=False)
+        cols = rng.integers(0, m, size=rows.size)
+        full[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()] = \
+            torch.from_numpy(rng.integers(1, 7, size=rows.size).astype(np.int32)).cuda()
+        full[:, m:] = 5                        # beyond the row end: ignored
+        flags = torch.full((n,), 9, dtype=torch.uint8, device="cuda")
+        _device.code_rows(full[:, :m], flags)
+        want = np.zeros(n, np.uint8)
+        want[rows] = 1
+        assert np.array_equal(flags.cpu().numpy(), want), (n, m, ld)
+
+    bad = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    good = corpus_columns[:, :70]
+    times = np.array(failure_table["times"] + [4000.0])
+    # scattered failing rows (> MAX_RUNS runs): whole-plane copy
+    many = np.concatenate([np.concatenate([good[:, i:i + 1], bad[:, :1]], axis=1)
+                           for i in range(70)], axis=1)
+    for cols_ in (many, np.concatenate([bad, good], axis=1)):
+        sats = pkg.init_batch(cols_)
+        host = pkg.propagate_batch(sats, times)
+        dev = pkg.propagate_batch_device(sats, times)
+        assert np.count_nonzero(host.error) > 0
+        assert np.array_equal(host.error, dev.error.cpu().numpy())
+    # same shape, no failing rows: the pooled block that held codes is reused
+    n_prev = host.n
+    del host
+    clean = pkg.init_batch(corpus_columns[:, 100:100 + n_prev])
+    reuses = _hostmem.stats()["reuses"]
+    host = pkg.propagate_batch(clean, times)
+    assert _hostmem.stats()["reuses"] > reuses
+    want = pkg.propagate_batch_device(clean, times).error.cpu().numpy()
+    assert np.array_equal(host.error, want)
 
 
 @pytest.mark.parametrize("n,m", [(1, 1_000_000), (200_000, 1), (3, 130)])

@@ -31,3 +31,19 @@ for _ in range(R):
         acc[k] = acc.get(k, 0.0) + v / R
     del res
 print(json.dumps({k: round(v * 1e3, 3) for k, v in acc.items()}, indent=1))
+
+# raw DMA floors into the same kind of pinned block
+from paper_2603_27830_b200 import _hostmem                         # noqa: E402
+dev = torch.device("cuda")
+for label, nbytes in (("planes_224MB", 6 * 9341 * 1000 * 4), ("grid_261MB", 7 * 9341 * 1000 * 4)):
+    src = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    dst = torch.from_numpy(np.asarray(_hostmem.alloc(nbytes))[:nbytes].view(np.float32))
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(R):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / R
+    print(f"{label}: {dt * 1e3:.3f} ms = {nbytes / dt / 1e9:.1f} GB/s")
