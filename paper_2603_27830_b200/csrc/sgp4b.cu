@@ -1504,6 +1504,30 @@ __device__ int epoch_code(const double* f, double ao, const Grav& g) {
   return bad_nm ? 2 : bad_em ? 1 : bad_pl ? 4 : (mrt < 1.0) ? 6 : 0;
 }
 
+// true when the epoch evaluation (epoch_code) provably returns 0, from
+// bounds that hold for every E: with el = |(axnl, aynl)| <= em +
+// |aycof| / pl_lp =: elb, ecose <= el gives rl >= am (1 - elb), pl >= am
+// (1 - elb^2) bounds temp1 = j2/2/pl and temp2 = temp1/pl, and betal,
+// cos2u lie in [0, 1] and [-1, 1], so (kernel.py:495-502)
+//   mrt >= am (1 - elb) (1 - 1.5 temp2 |con41|) - temp1/2 |x1mth2|,
+// and pl > 0.  A margin of 1e-6 covers the rounding of both evaluations.
+// Every ordinary orbit passes and skips the Kepler loop; anything near a
+// threshold (or outside 1e-6 <= em < 0.5, or bad_nm) takes the exact path.
+__device__ __forceinline__ bool epoch_clear(const double* f, double ao, const Grav& g) {
+  const double em = f[F_ECCO];
+  if (!(f[F_NO_UNKOZAI] > 0.0) || !(em >= 1.0e-6 && em < 0.5) || !(ao > 0.0)) return false;
+  const double tlp = 1.0 / (ao * (1.0 - em * em));
+  const double elb = em + tlp * fabs(f[F_AYCOF]);
+  if (!(elb < 0.5)) return false;
+  const double plmin = ao * (1.0 - elb * elb);
+  const double t1 = 0.5 * fabs(g.j2) / plmin;
+  const double t2 = t1 / plmin;
+  const double k = 1.5 * t2 * fabs(f[F_CON41]);
+  if (!(k < 1.0)) return false;
+  const double lb = ao * (1.0 - elb) * (1.0 - k) - 0.5 * t1 * fabs(f[F_X1MTH2]);
+  return lb > 1.0 + 1.0e-6;
+}
+
 __device__ void init_one(const double el[7], const Grav& g, double* f, double* v, int& code,
                          bool& isimp_out) {
   const double tiny = DBL_MIN;
@@ -1639,7 +1663,7 @@ __device__ void init_one(const double el[7], const Grav& g, double* f, double* v
   const double ao_sc[3] = {ao, sinio, cosio};
   record_values(f, g, v, ao_sc);
   // epoch evaluation  :316-322
-  if (code == 0) code = epoch_code(f, ao, g);
+  if (code == 0 && !epoch_clear(f, ao, g)) code = epoch_code(f, ao, g);
 }
 
 // One warp per block (the fp64 chains are long and latency-bound: spreading

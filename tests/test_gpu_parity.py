@@ -723,6 +723,30 @@ def test_sparse_code_rows_with_errors(failure_table, corpus_columns, precision):
     assert summary.nonzero_error_count == int(np.count_nonzero(host.error))
 
 
+@pytest.mark.parametrize("precision", [64, 32])
+def test_epoch_code_near_decay_threshold(oracle, precision):
+    """Init codes across the epoch decay threshold (mrt = 1 earth radius at
+    t = 0) and at larger eccentricities: the init kernel's bound that lets
+    ordinary orbits skip the exact epoch evaluation (epoch_clear) never
+    changes a code.  Perigees sweep 0.97..1.03 earth radii."""
+    pkg = _gpu()
+    rng = np.random.default_rng(11)
+    n = 4000
+    ecc = np.concatenate([rng.uniform(1e-6, 2e-3, n // 2), rng.uniform(2e-3, 0.45, n // 2)])
+    rp = rng.uniform(0.97, 1.03, n)                       # perigee radius, earth radii
+    a = rp / (1.0 - ecc)
+    xke = 0.07436691613317342                             # WGS72 (gravity.py)
+    no = xke / a ** 1.5
+    cols = np.stack([no, ecc, rng.uniform(0, np.pi, n), rng.uniform(0, 2 * np.pi, n),
+                     rng.uniform(0, 2 * np.pi, n), rng.uniform(0, 2 * np.pi, n),
+                     rng.uniform(-1e-3, 1e-3, n)])
+    sats = pkg.init_batch(cols, precision=precision)
+    want = np.asarray(oracle.init_columns(cols, 64)["error_code_at_init"])
+    got = np.asarray(sats.error_codes)
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+    assert (want == 6).sum() > 100 and (want == 0).sum() > 100
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
