@@ -85,7 +85,9 @@ int sgp4b_pack(const double* satrec_dev, const int32_t* init_code_dev,
  *                class (drag over long or backward spans) with the general
  *                path; the bound tells the kernel which rows can have such
  *                cells.  INFINITY or NaN is always correct (every row of a
- *                fixed class gets the check), only slower; fp64 ignores it. */
+ *                fixed class gets the check), only slower; fp64 ignores it.
+ *   m is at most 2^30 (columns are indexed with 32-bit offsets; longer
+ *   rows are split by the caller). */
 int sgp4b_propagate_grid(const void* record_dev, int64_t n,
                          const void* times_dev, const float* times_lo_dev,
                          int64_t m, double t_absmax, int precision,

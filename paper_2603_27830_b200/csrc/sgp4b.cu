@@ -1815,6 +1815,17 @@ __device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
 #ifndef SGP4B_VEC
 #define SGP4B_VEC 4
 #endif
+#ifndef SGP4B_ROW32
+#define SGP4B_ROW32 1
+#endif
+#ifndef SGP4B_UNIFORM_W
+#define SGP4B_UNIFORM_W 1
+#endif
+#ifndef SGP4B_ROWPTR
+#define SGP4B_ROWPTR 1
+#endif
+// longest row the kernels index with 32-bit column offsets
+constexpr int64_t kMaxSteps = (int64_t)1 << 30;
 constexpr int kVec = SGP4B_VEC;     // cells advanced in lockstep (2 = one packed pair)
 static_assert(kCellsPerLane % kVec == 0 && kVec % 2 == 0, "fp32 cells run in packed pairs");
 
@@ -1852,32 +1863,48 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
                                          const float* __restrict__ times_lo, int64_t m,
                                          T* __restrict__ row, int64_t plane_stride,
                                          int32_t* __restrict__ crow, float t_crit) {
+  // column indices: 32-bit (the ABI rejects m > kMaxSteps), so bounds tests
+  // and increments are single ALU ops
+  using J = typename std::conditional<SGP4B_ROW32 != 0, unsigned, int64_t>::type;
+  const J mj = (J)m;
   // a lane's kCellsPerLane times at column j (zero past the row end)
-  auto load_times = [&](int64_t j, T (&th)[kCellsPerLane], float (&tl)[kCellsPerLane]) {
-    if (VEC && j + kCellsPerLane <= m) {
+  auto load_times = [&](J j, T (&th)[kCellsPerLane], float (&tl)[kCellsPerLane]) {
+    if (VEC && j + kCellsPerLane <= mj) {
       ld_vec<kCellsPerLane>(times + j, th);
     } else {
 #pragma unroll
-      for (int k = 0; k < kCellsPerLane; ++k) th[k] = j + k < m ? __ldg(times + j + k) : T(0);
+      for (int k = 0; k < kCellsPerLane; ++k) th[k] = j + k < mj ? __ldg(times + j + k) : T(0);
     }
 #pragma unroll
-    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j + k < m) ? __ldg(times_lo + j + k) : 0.0f;
+    for (int k = 0; k < kCellsPerLane; ++k) tl[k] = (LO && j + k < mj) ? __ldg(times_lo + j + k) : 0.0f;
   };
-  int64_t j0 = c0 * kCellsPerWarp + lane * kCellsPerLane;
+  J j0 = (J)(c0 * kCellsPerWarp) + (J)(lane * kCellsPerLane);
   T th[kCellsPerLane];
   float tl[kCellsPerLane];
   load_times(j0, th, tl);
+#if SGP4B_ROWPTR
+  // per-plane row bases (warp-uniform); a store address is base + j0
+  T* rp[6];
+#pragma unroll
+  for (int p = 0; p < 6; ++p) rp[p] = row + p * plane_stride;
+#define SGP4B_PADDR(p, k) (rp[p] + (j0 + (k)))
+#define SGP4B_CADDR(k) (crow + (j0 + (k)))
+#else
   T* pb = row + j0;                          // output pointers walk the row
   int32_t* cb = crow + j0;
-  for (int64_t c = c0; c < c1; ++c, j0 += kCellsPerWarp) {
+#define SGP4B_PADDR(p, k) (pb + (p) * plane_stride + (k))
+#define SGP4B_CADDR(k) (cb + (k))
+#endif
+  const J jc1 = (J)(c1 * kCellsPerWarp);
+  for (J jc = (J)(c0 * kCellsPerWarp); jc < jc1; jc += kCellsPerWarp, j0 += kCellsPerWarp) {
 #if SGP4B_SHFL_REC
     // keep the warp converged (record fields are shuffled): lanes past the
     // row end compute a dummy cell and skip the stores
-    if (__all_sync(0xffffffffu, j0 >= m)) break;
+    if (__all_sync(0xffffffffu, j0 >= mj)) break;
 #else
-    if (j0 >= m) break;                     // only the row's last chunk is partial
+    if (j0 >= mj) break;                    // only the row's last chunk is partial
 #endif
-    const bool full = VEC && j0 + kCellsPerLane <= m;
+    const bool full = VEC && j0 + kCellsPerLane <= mj;
     // the next chunk's times are loaded before this chunk's cells run, so
     // their latency hides behind the cell math
     T thn[kCellsPerLane];
@@ -1890,14 +1917,16 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     if constexpr (MASKED) {
 #pragma unroll
       for (int k = 0; k < kCellsPerLane; ++k) {
-        if (fabsf((float)th[k]) > t_crit && j0 + k < m) {
+        if (fabsf((float)th[k]) > t_crit && j0 + k < mj) {
 #pragma unroll
-          for (int p = 0; p < 6; ++p) st_cs(pb + p * plane_stride + k, out[p][k]);
-          st_cs(cb + k, code[k]);
+          for (int p = 0; p < 6; ++p) st_cs(SGP4B_PADDR(p, k), out[p][k]);
+          st_cs(SGP4B_CADDR(k), code[k]);
         }
       }
+#if !SGP4B_ROWPTR
       pb += kCellsPerWarp;
       cb += kCellsPerWarp;
+#endif
 #pragma unroll
       for (int k = 0; k < kCellsPerLane; ++k) {
         th[k] = thn[k];
@@ -1926,21 +1955,33 @@ __device__ __forceinline__ void row_loop(const CellsFn& cells, int64_t c0, int64
     }
 #endif
 
+#if !SGP4B_ROWPTR
     T* base = pb;
     int32_t* cbase = cb;
     pb += kCellsPerWarp;
     cb += kCellsPerWarp;
+#endif
     if (full) {
 #pragma unroll
+#if SGP4B_ROWPTR
+      for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(rp[p] + j0, out[p]);
+      st_vec_cs<kCellsPerLane>(crow + j0, code);
+#else
       for (int p = 0; p < 6; ++p) st_vec_cs<kCellsPerLane>(base + p * plane_stride, out[p]);
       st_vec_cs<kCellsPerLane>(cbase, code);
+#endif
     } else {
 #pragma unroll
       for (int k = 0; k < kCellsPerLane; ++k) {
-        if (j0 + k < m) {
+        if (j0 + k < mj) {
 #pragma unroll
+#if SGP4B_ROWPTR
+          for (int p = 0; p < 6; ++p) st_cs(rp[p] + (j0 + k), out[p][k]);
+          st_cs(crow + (j0 + k), code[k]);
+#else
           for (int p = 0; p < 6; ++p) st_cs(base + p * plane_stride + k, out[p][k]);
           st_cs(cbase + k, code[k]);
+#endif
         }
       }
     }
@@ -2146,7 +2187,15 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
             int32_t* __restrict__ codes, int64_t code_stride, int64_t chunks, float t_absmax) {
   constexpr int kBlock = grid_block<T>();
   const int64_t nwarps = (int64_t)gridDim.x * (kBlock / 32);
+#if SGP4B_UNIFORM_W
+  // the warp index through a lane-0 shuffle: the compiler then knows it (and
+  // every row/chunk bound and row base pointer derived from it) is
+  // warp-uniform and can keep them in uniform registers
+  const int64_t w = (int64_t)blockIdx.x * (kBlock / 32) +
+                    __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+#else
   const int64_t w = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t total = n * chunks;
   const int64_t g0 = total * w / nwarps;
@@ -2430,6 +2479,9 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n, const void* times_de
     return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: precision must be 32 or 64, got %d", precision);
   if (!record_dev || !times_dev || !planes_dev || !codes_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: null pointer argument");
+  if (m > kMaxSteps)
+    return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: m = %lld exceeds 2^30 steps per row",
+                (long long)m);
   if (row_stride < m || code_stride < m || plane_stride < (n - 1) * row_stride + m)
     return fail(SGP4B_EINVAL, "sgp4b_propagate_grid: strides overlap the grid");
   const size_t esz = precision == 64 ? 8 : 4;

@@ -58,6 +58,8 @@ GRAV = np.zeros(8)
     lambda L: L.sgp4b_pack(1, 1, 1, 4, None, 64, 1, None),                      # null grav
     lambda L: L.sgp4b_propagate_grid(1, 4, 1, None, 0, 1.0, 32, GRAV.ctypes.data, 1, 0, 0, 1, 0, None),
     lambda L: L.sgp4b_propagate_grid(1, 4, 1, None, 8, 1.0, 32, GRAV.ctypes.data, 1, 8, 4, 1, 8, None),
+    lambda L: L.sgp4b_propagate_grid(1, 1, 1, None, (1 << 30) + 1, 1.0, 32, GRAV.ctypes.data, 1,
+                                     (1 << 31), (1 << 31), 1, (1 << 31), None),  # m > 2^30
     lambda L: L.sgp4b_propagate_pairs(1, 1, 1, None, 0, 1.0, 64, GRAV.ctypes.data, 1, 1, None),
     lambda L: L.sgp4b_solve_kepler(1, 1, 1, 4, 8, 1, None),
     lambda L: L.sgp4b_code_rows(1, 0, 4, 4, 1, None),                           # n = 0
