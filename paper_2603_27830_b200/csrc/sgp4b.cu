@@ -1824,6 +1824,9 @@ __device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
 #ifndef SGP4B_ROWPTR
 #define SGP4B_ROWPTR 1
 #endif
+#ifndef SGP4B_REC64_REGS
+#define SGP4B_REC64_REGS 0
+#endif
 // longest row the kernels index with 32-bit column offsets
 constexpr int64_t kMaxSteps = (int64_t)1 << 30;
 constexpr int kVec = SGP4B_VEC;     // cells advanced in lockstep (2 = one packed pair)
@@ -2089,8 +2092,8 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const float* recg, con
 #endif
 constexpr int kIlp64 = SGP4B_F64_ILP;
 
-template <bool FAST, bool ISIMP>
-__device__ __forceinline__ void row64(const RecS<double>& R, const TrigGrid& tr, double re,
+template <bool FAST, bool ISIMP, class RT>
+__device__ __forceinline__ void row64(const RT& R, const double* recp, const TrigGrid& tr, double re,
                                       double vkm, int64_t c0, int64_t c1, int lane,
                                       const double* __restrict__ times, int64_t m,
                                       double* __restrict__ row, int64_t ps,
@@ -2125,7 +2128,7 @@ __device__ __forceinline__ void row64(const RecS<double>& R, const TrigGrid& tr,
       const unsigned jj = j + 32 * i;
       if (jj >= jend) break;
       if (!ok[i]) {
-        cell64_fallback(R.p, t[i], re, vkm, tr.tab, row + jj, ps, crow + jj);
+        cell64_fallback(recp, t[i], re, vkm, tr.tab, row + jj, ps, crow + jj);
         continue;
       }
 #ifndef SGP4B_NOSTORE
@@ -2143,7 +2146,8 @@ __device__ __forceinline__ void row64(const RecS<double>& R, const TrigGrid& tr,
   }
 }
 
-__device__ __forceinline__ void dispatch_row64(const RecS<double>& R, const TrigGrid& tr,
+template <class RT>
+__device__ __forceinline__ void dispatch_row64(const RT& R, const double* recp, const TrigGrid& tr,
                                                const Grav& g, int64_t c0, int64_t c1, int lane,
                                                const double* times, int64_t m, double* row,
                                                int64_t ps, int32_t* crow) {
@@ -2151,11 +2155,11 @@ __device__ __forceinline__ void dispatch_row64(const RecS<double>& R, const Trig
   const bool fast = ((flags >> KEPLER_SHIFT) & 0xf) == 1;
   if (fast) {
     if (flags & FLAG_ISIMP)
-      row64<true, true>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+      row64<true, true>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
     else
-      row64<true, false>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+      row64<true, false>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
   } else {
-    row64<false, false>(R, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+    row64<false, false>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
   }
 }
 
@@ -2201,7 +2205,8 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
   const int64_t g0 = total * w / nwarps;
   const int64_t g1 = total * (w + 1) / nwarps;
 
-  constexpr bool kSmem = sizeof(T) == 8 ? true : SGP4B_SMEM_REC;   // fp64: records in smem
+  // fp64: records in shared memory unless SGP4B_REC64_REGS
+  constexpr bool kSmem = sizeof(T) == 8 ? !SGP4B_REC64_REGS : SGP4B_SMEM_REC;
   constexpr bool kShfl = sizeof(T) == 4 && SGP4B_SHFL_REC;
   __shared__ __align__(16) T srec[kSmem ? kBlock / 32 : 1][S_COUNT];
   T* my = srec[kSmem ? (threadIdx.x >> 5) : 0];
@@ -2250,7 +2255,10 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
     if (rec_idx == nullptr && gi + (c1 - c0) < g1 && lane < (int)(S_COUNT * sizeof(T) + 127) / 128)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (ri + 1) * S_COUNT + lane * (128 / sizeof(T))));
     if constexpr (sizeof(T) == 8) {
-      dispatch_row64(R, TrigGrid{sintab}, g, c0, c1, lane, times + sat * times_ld, m,
+      const double* recp;
+      if constexpr (kSmem) recp = reinterpret_cast<const double*>(my);
+      else recp = reinterpret_cast<const double*>(rec) + ri * S_COUNT;
+      dispatch_row64(R, recp, TrigGrid{sintab}, g, c0, c1, lane, times + sat * times_ld, m,
                      planes + sat * row_stride, plane_stride, codes + sat * code_stride);
     } else {
       dispatch_row<VEC, LO>(R, reinterpret_cast<const float*>(rec) + ri * S_COUNT, g, c0, c1,
