@@ -326,12 +326,15 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
                 for p in range(6):
                     torch.from_numpy(planes_h[p, lo:hi]).copy_(planes[p], non_blocking=True)
             jobs.append((stream, codes, sub, t_d, planes, error))
-    for stream, codes, *_ in jobs:
-        with torch.cuda.stream(stream):
-            codes.finish()
-    for stream, codes, *_ in jobs:
-        stream.synchronize()
-        codes.join()
+    try:
+        for stream, codes, *_ in jobs:
+            with torch.cuda.stream(stream):
+                codes.finish()
+        for stream, *_ in jobs:
+            stream.synchronize()
+    finally:
+        for _, codes, *_ in jobs:
+            codes.join()
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
 
 
@@ -359,10 +362,12 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None,
         t_d = torch.from_numpy(t).to(dev.device, non_blocking=True)
         res = propagate_batch_device(sats, t_d, t_absmax=_device.times_absmax(t))
         codes = _CodesToHost(res.error, error_h, flags_h, stream)
-        torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
-        codes.finish()
-        stream.synchronize()
-        codes.join()
+        try:
+            torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
+            codes.finish()
+            stream.synchronize()
+        finally:
+            codes.join()            # no fill may outlive the call (the block is pooled)
     _last_transfer.update(d2h_bytes=planes_h.nbytes + codes.d2h_bytes,
                           code_bytes_zero_filled=error_h.nbytes - (codes.d2h_bytes - flags_h.nbytes))
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
@@ -424,9 +429,12 @@ class _CodesToHost:
         self.fills += _hostmem.zero_fill_async(self.error_h, lo, n)
 
     def join(self) -> None:
-        for f in self.fills:
-            f.result()
-        self.fills = []
+        """Wait for every zero fill (all of them, even if one raised)."""
+        fills, self.fills = self.fills, []
+        errors = [f.exception() for f in fills]
+        for e in errors:
+            if e is not None:
+                raise e
 
 
 def _host_grid(n: int, m: int, precision: int):
