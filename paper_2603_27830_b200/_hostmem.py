@@ -150,12 +150,24 @@ _ZERO_CHUNK = 4 << 20
 _fill_pool = None
 
 
+def pool_threads() -> int:
+    """Host threads for zero fills and staged copies (``SGP4B_HOST_THREADS``,
+    default: every core the process may use, at most 32)."""
+    v = os.environ.get("SGP4B_HOST_THREADS")
+    if v:
+        return max(1, int(v))
+    try:
+        n = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        n = os.cpu_count() or 2
+    return max(1, min(32, n))
+
+
 def _pool():
     global _fill_pool
     if _fill_pool is None:
         from concurrent.futures import ThreadPoolExecutor
-        _fill_pool = ThreadPoolExecutor(max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)),
-                                        thread_name_prefix="sgp4b-zero")
+        _fill_pool = ThreadPoolExecutor(max_workers=pool_threads(), thread_name_prefix="sgp4b-host")
     return _fill_pool
 
 

@@ -10,6 +10,7 @@ multi-GPU sharding and the throughput benchmark use.
 
 from __future__ import annotations
 
+import ctypes
 import struct
 import sys
 from dataclasses import dataclass
@@ -356,18 +357,30 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None,
     t = _times(sats, times)
     dev = sats.device_satrec
     n, m = sats.n, t.size
-    planes_h, error_h, flags_h = _host_grid(n, m, dev.precision)
+    itemsize = 4 if dev.precision == 32 else 8
+    staged = n * m * (6 * itemsize + 4) > _hostmem.cache_limit()
+    planes_h, error_h, flags_h = (_host_grid_pageable if staged else _host_grid)(n, m,
+                                                                                 dev.precision)
     with torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
         t_d = torch.from_numpy(t).to(dev.device, non_blocking=True)
         res = propagate_batch_device(sats, t_d, t_absmax=_device.times_absmax(t))
-        codes = _CodesToHost(res.error, error_h, flags_h, stream)
+        stager = _StagedD2H(stream) if staged else None
+        codes = _CodesToHost(res.error, error_h, flags_h, stream, stager)
         try:
-            torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
+            if stager is not None:
+                for p in range(6):
+                    stager.copy(res.planes[p], planes_h[p])
+            else:
+                torch.from_numpy(planes_h).copy_(res.planes, non_blocking=True)
             codes.finish()
+            if stager is not None:
+                stager.join()
             stream.synchronize()
         finally:
             codes.join()            # no fill may outlive the call (the block is pooled)
+            if stager is not None:
+                stager.join()
     _last_transfer.update(d2h_bytes=planes_h.nbytes + codes.d2h_bytes,
                           code_bytes_zero_filled=error_h.nbytes - (codes.d2h_bytes - flags_h.nbytes))
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
@@ -396,8 +409,10 @@ class _CodesToHost:
 
     MAX_RUNS = 64
 
-    def __init__(self, error_d: torch.Tensor, error_h: np.ndarray, flags_h: np.ndarray, stream):
+    def __init__(self, error_d: torch.Tensor, error_h: np.ndarray, flags_h: np.ndarray, stream,
+                 stager: "_StagedD2H | None" = None):
         self.error_d, self.error_h, self.flags_h, self.stream = error_d, error_h, flags_h, stream
+        self.stager = stager
         self.fills = []
         n = error_d.shape[0]
         flags_d = torch.empty(n, dtype=torch.uint8, device=error_d.device)
@@ -423,7 +438,10 @@ class _CodesToHost:
         self.d2h_bytes = self.flags_h.nbytes + sum(b - a for a, b in runs) * row_bytes
         lo = 0
         for a, b in runs:
-            torch.from_numpy(self.error_h[a:b]).copy_(self.error_d[a:b], non_blocking=True)
+            if self.stager is not None:
+                self.stager.copy(self.error_d[a:b], self.error_h[a:b])
+            else:
+                torch.from_numpy(self.error_h[a:b]).copy_(self.error_d[a:b], non_blocking=True)
             self.fills += _hostmem.zero_fill_async(self.error_h, lo, a)
             lo = b
         self.fills += _hostmem.zero_fill_async(self.error_h, lo, n)
@@ -432,6 +450,88 @@ class _CodesToHost:
         """Wait for every zero fill (all of them, even if one raised)."""
         fills, self.fills = self.fills, []
         errors = [f.exception() for f in fills]
+        for e in errors:
+            if e is not None:
+                raise e
+
+
+def _host_grid_pageable(n: int, m: int, precision: int):
+    """Pageable (6, n, m) planes + (n, m) codes, as the reference allocates
+    them (batch.py:177-183), for grids above the pinned pool's cache limit:
+    page-locking a multi-GB block costs ~0.4 s/GB, far more than staging
+    through pinned buffers.  The row flags stay pinned (tiny)."""
+    try:
+        planes = np.empty((6, n, m), dtype=_device.np_dtype(precision))
+        error = np.empty((n, m), dtype=np.int32)
+    except MemoryError:
+        itemsize = 4 if precision == 32 else 8
+        raise GridAllocationError(n, m, 6 * n * m * itemsize + 4 * n * m) from None
+    flags = _hostmem.empty([((n,), np.uint8)])[0]
+    return planes, error, flags
+
+
+class _StagedD2H:
+    """Device -> pageable host copies through a ring of pinned staging
+    buffers: piece k crosses PCIe into buffer k mod R while worker threads
+    move the earlier pieces into place (``ctypes.memmove`` releases the GIL),
+    so the DMA and the host copies (page faults included) overlap.  Sources
+    and destinations are C-contiguous; ``join`` waits for every piece."""
+
+    PIECE = 32 << 20
+    RING = 24
+
+    def __init__(self, stream):
+        self.stream = stream
+        self.ring = [np.asarray(_hostmem.alloc(self.PIECE)) for _ in range(self.RING)]
+        self.events = [torch.cuda.Event() for _ in range(self.RING)]
+        self.pending = [None] * self.RING
+        self.k = 0
+
+    @staticmethod
+    def _drain(event, buf, dst_addr, nbytes):
+        event.synchronize()
+        ctypes.memmove(dst_addr, buf.ctypes.data, nbytes)
+
+    def _piece(self, src: torch.Tensor, dst_addr: int, nbytes: int) -> None:
+        """One D2H of ``src`` (any strides; ``nbytes`` of payload) into the
+        next staging buffer, then an async move to ``dst_addr``."""
+        k = self.k
+        self.k = (k + 1) % self.RING
+        if self.pending[k] is not None:
+            self.pending[k].result()                # buffer k drained
+        buf = self.ring[k]
+        view = torch.from_numpy(buf[:nbytes]).view(src.dtype).view(src.shape)
+        view.copy_(src, non_blocking=True)
+        self.events[k].record(self.stream)
+        self.pending[k] = _hostmem._pool().submit(self._drain, self.events[k], buf, dst_addr,
+                                                  nbytes)
+
+    def copy(self, src: torch.Tensor, dst: np.ndarray) -> None:
+        """``src`` (rows, cols) on the device with unit column stride (row
+        stride free: padded grids), ``dst`` the C-contiguous host rows."""
+        if src.dim() != 2 or src.stride(1) != 1 or not dst.flags.c_contiguous \
+                or tuple(src.shape) != dst.shape or src.element_size() != dst.itemsize:
+            raise ValueError("staged copy: (rows, cols) source with unit column stride and a "
+                             "C-contiguous destination of the same shape and item size")
+        rows, cols = dst.shape
+        row_bytes = cols * dst.itemsize
+        base = dst.ctypes.data
+        if row_bytes <= self.PIECE:
+            step = self.PIECE // row_bytes
+            for r0 in range(0, rows, step):
+                r1 = min(rows, r0 + step)
+                self._piece(src[r0:r1], base + r0 * row_bytes, (r1 - r0) * row_bytes)
+        else:
+            step = self.PIECE // dst.itemsize
+            for r in range(rows):
+                for c0 in range(0, cols, step):
+                    c1 = min(cols, c0 + step)
+                    self._piece(src[r:r + 1, c0:c1], base + r * row_bytes + c0 * dst.itemsize,
+                                (c1 - c0) * dst.itemsize)
+
+    def join(self) -> None:
+        pending, self.pending = self.pending, [None] * self.RING
+        errors = [f.exception() for f in pending if f is not None]
         for e in errors:
             if e is not None:
                 raise e

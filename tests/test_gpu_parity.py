@@ -750,6 +750,30 @@ def test_epoch_code_near_decay_threshold(oracle, precision):
     assert (want == 6).sum() > 100 and (want == 0).sum() > 100
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_staged_pageable_result_equals_device(failure_table, corpus_columns, precision,
+                                              monkeypatch):
+    """Grids above the pinned pool's cache limit come back in pageable
+    arrays through the pinned staging ring (pieces smaller than the grid, so
+    the ring wraps); planes and codes equal the device grid bit for bit,
+    with failing rows mixed in."""
+    import torch
+    pkg = _gpu()
+    from paper_2603_27830_b200 import batch as batch_mod
+    monkeypatch.setenv("SGP4B_HOST_CACHE_BYTES", "1")
+    monkeypatch.setattr(batch_mod._StagedD2H, "PIECE", 1 << 16)
+    monkeypatch.setattr(batch_mod._StagedD2H, "RING", 3)
+    bad = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    cols = np.concatenate([corpus_columns[:, :300], bad, corpus_columns[:, 300:400]], axis=1)
+    times = np.linspace(-100.0, 3000.0, 257)
+    sats = pkg.init_batch(cols, precision=precision)
+    host = pkg.propagate_batch(sats, times)
+    dev = pkg.propagate_batch_device(sats, times)
+    assert np.count_nonzero(host.error) > 0
+    assert np.array_equal(host.error, dev.error.cpu().numpy())
+    assert np.array_equal(host.planes.view(np.uint8), dev.planes.cpu().numpy().view(np.uint8))
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
