@@ -304,13 +304,19 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
     dev = sats.device_satrec
     n, m = sats.n, t.size
     devs = _devices(devices)
-    planes_h, error_h, flags_h = _host_grid(n, m, dev.precision)
+    itemsize = 4 if dev.precision == 32 else 8
+    staged = n * m * (6 * itemsize + 4) > _hostmem.cache_limit()
+    planes_h, error_h, flags_h = (_host_grid_pageable if staged else _host_grid)(n, m,
+                                                                                 dev.precision)
     t_abs = _device.times_absmax(t)
     src_stream = torch.cuda.current_stream(dev.device)
     ready = torch.cuda.Event()
     ready.record(src_stream)                  # the records exist on the source device
     jobs = []
     from .shard import shard_bounds
+    # every device's grid kernel and code-row flags are queued first, so the
+    # kernels run concurrently; the copies follow (a staged copy may block
+    # the host while its ring cycles)
     for g, d in enumerate(devs):
         lo, hi = shard_bounds(n, len(devs), g)
         if hi <= lo:
@@ -323,19 +329,30 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
                 t_d = torch.from_numpy(t).to(d, non_blocking=True)
                 planes, error = _alloc_grid(hi - lo, m, dev.precision, d)
                 _device.propagate_grid(sub, t_d, planes, error, t_absmax=t_abs)
-                codes = _CodesToHost(error, error_h[lo:hi], flags_h[lo:hi], stream)
-                for p in range(6):
-                    torch.from_numpy(planes_h[p, lo:hi]).copy_(planes[p], non_blocking=True)
-            jobs.append((stream, codes, sub, t_d, planes, error))
+                stager = _StagedD2H(stream, ring=max(4, _StagedD2H.RING // len(devs))) \
+                    if staged else None
+                codes = _CodesToHost(error, error_h[lo:hi], flags_h[lo:hi], stream, stager)
+            jobs.append((stream, codes, stager, lo, hi, sub, t_d, planes, error))
     try:
+        for stream, codes, stager, lo, hi, sub, t_d, planes, error in jobs:
+            with torch.cuda.device(stream.device), torch.cuda.stream(stream):
+                for p in range(6):
+                    if stager is not None:
+                        stager.copy(planes[p], planes_h[p, lo:hi])
+                    else:
+                        torch.from_numpy(planes_h[p, lo:hi]).copy_(planes[p], non_blocking=True)
         for stream, codes, *_ in jobs:
-            with torch.cuda.stream(stream):
+            with torch.cuda.device(stream.device), torch.cuda.stream(stream):
                 codes.finish()
-        for stream, *_ in jobs:
+        for stream, codes, stager, *_ in jobs:
+            if stager is not None:
+                stager.join()
             stream.synchronize()
     finally:
-        for _, codes, *_ in jobs:
+        for _, codes, stager, *_ in jobs:
             codes.join()
+            if stager is not None:
+                stager.join()
     return BatchResult(planes=planes_h, error=error_h, n=n, m=m)
 
 
@@ -480,11 +497,12 @@ class _StagedD2H:
     PIECE = 32 << 20
     RING = 24
 
-    def __init__(self, stream):
+    def __init__(self, stream, ring: int | None = None):
         self.stream = stream
-        self.ring = [np.asarray(_hostmem.alloc(self.PIECE)) for _ in range(self.RING)]
-        self.events = [torch.cuda.Event() for _ in range(self.RING)]
-        self.pending = [None] * self.RING
+        self.nring = ring or self.RING
+        self.ring = [np.asarray(_hostmem.alloc(self.PIECE)) for _ in range(self.nring)]
+        self.events = [torch.cuda.Event() for _ in range(self.nring)]
+        self.pending = [None] * self.nring
         self.k = 0
 
     @staticmethod
@@ -496,7 +514,7 @@ class _StagedD2H:
         """One D2H of ``src`` (any strides; ``nbytes`` of payload) into the
         next staging buffer, then an async move to ``dst_addr``."""
         k = self.k
-        self.k = (k + 1) % self.RING
+        self.k = (k + 1) % self.nring
         if self.pending[k] is not None:
             self.pending[k].result()                # buffer k drained
         buf = self.ring[k]
@@ -530,7 +548,7 @@ class _StagedD2H:
                                 (c1 - c0) * dst.itemsize)
 
     def join(self) -> None:
-        pending, self.pending = self.pending, [None] * self.RING
+        pending, self.pending = self.pending, [None] * self.nring
         errors = [f.exception() for f in pending if f is not None]
         for e in errors:
             if e is not None:

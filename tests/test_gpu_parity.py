@@ -925,18 +925,28 @@ def test_hand_built_init_code_persists(real_elements, precision, dtype):
     assert st.error_code.tolist() == [300, 300, 300]
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("precision", [32, 64])
 @pytest.mark.parametrize("ndev", [2, 3])
-def test_multi_device_path_bitwise(corpus_columns, precision, ndev):
+def test_multi_device_path_bitwise(corpus_columns, failure_table, precision, ndev, staged,
+                                   monkeypatch):
     """propagate_batch(devices=...) — satellite ranges on several GPUs of
-    one process, each D2H-ing into one pinned host grid — equals the
-    single-device grid bit for bit.  On a 1-GPU box the "devices" are the
-    same GPU named several times (separate streams, same code path)."""
+    one process, each D2H-ing into one host grid (pinned, or pageable
+    through per-device staging rings when the grid exceeds the pinned cache
+    limit) — equals the single-device grid bit for bit.  On a 1-GPU box the
+    "devices" are the same GPU named several times (separate streams, same
+    code path)."""
     import torch
     pkg = _gpu()
-    sats = pkg.init_batch(corpus_columns[:, :257], precision=precision)
+    from paper_2603_27830_b200 import batch as batch_mod
+    bad = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    cols = np.concatenate([corpus_columns[:, :200], bad, corpus_columns[:, 200:257]], axis=1)
+    sats = pkg.init_batch(cols, precision=precision)
     times = np.linspace(-60.0, 2880.0, 131)
     single = pkg.propagate_batch(sats, times)
+    if staged:
+        monkeypatch.setenv("SGP4B_HOST_CACHE_BYTES", "1")
+        monkeypatch.setattr(batch_mod._StagedD2H, "PIECE", 1 << 14)
     devs = [i % torch.cuda.device_count() for i in range(ndev)]
     multi = pkg.propagate_batch(sats, times, devices=devs)
     assert np.array_equal(multi.planes, single.planes, equal_nan=True)
