@@ -161,6 +161,10 @@ def times_absmax(times) -> float:
     return max(float(t.max()), -float(t.min())) if t.size else 0.0
 
 
+#: longest row one grid launch takes (sgp4b.h)
+MAX_STEPS_PER_LAUNCH = 1 << 30
+
+
 def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,
                    codes: torch.Tensor, times_lo: torch.Tensor | None = None,
                    rows: tuple[int, int] | None = None, t_absmax: float | None = None) -> None:
@@ -181,11 +185,16 @@ def propagate_grid(dev: DeviceSatrec, times: torch.Tensor, planes: torch.Tensor,
         raise ValueError("output columns must be contiguous")
     rec = dev.record[r0:r1]
     g = _grav_host(dev.grav, dev.device)
-    _native.check(_native.load().sgp4b_propagate_grid(
-        rec.data_ptr(), n, times.data_ptr(), _native.ptr(times_lo), m, float(t_absmax),
-        dev.precision,
-        _host_ptr(g), planes.data_ptr(), planes.stride(0), planes.stride(1),
-        codes.data_ptr(), codes.stride(0), _stream(dev.device)))
+    # the kernels index columns with 32-bit offsets (sgp4b.h: m <= 2^30);
+    # longer rows run as column blocks of the same grid
+    for c0 in range(0, m, MAX_STEPS_PER_LAUNCH):
+        c1 = min(m, c0 + MAX_STEPS_PER_LAUNCH)
+        tl = times_lo[c0:c1] if times_lo is not None else None
+        _native.check(_native.load().sgp4b_propagate_grid(
+            rec.data_ptr(), n, times[c0:c1].data_ptr(), _native.ptr(tl), c1 - c0,
+            float(t_absmax), dev.precision, _host_ptr(g), planes[:, :, c0:].data_ptr(),
+            planes.stride(0), planes.stride(1), codes[:, c0:].data_ptr(), codes.stride(0),
+            _stream(dev.device)))
 
 
 def propagate_pairs(dev: DeviceSatrec, sat_idx: torch.Tensor, times: torch.Tensor,

@@ -774,6 +774,24 @@ def test_staged_pageable_result_equals_device(failure_table, corpus_columns, pre
     assert np.array_equal(host.planes.view(np.uint8), dev.planes.cpu().numpy().view(np.uint8))
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_long_rows_split_into_column_blocks(corpus_columns, precision, monkeypatch):
+    """Rows longer than one launch takes (2^30 steps) run as column blocks
+    of the same grid; with the block length forced down to 100 the grid is
+    bitwise equal to a single launch."""
+    import torch
+    pkg = _gpu()
+    from paper_2603_27830_b200 import _device
+    sats = pkg.init_batch(corpus_columns[:, :37], precision=precision)
+    times = np.linspace(-30.0, 2000.0, 1003)
+    whole = pkg.propagate_batch_device(sats, times)
+    monkeypatch.setattr(_device, "MAX_STEPS_PER_LAUNCH", 100)
+    split = pkg.propagate_batch_device(sats, times)
+    assert torch.equal(whole.error, split.error)
+    assert torch.equal(whole.planes.contiguous().view(torch.int8),
+                       split.planes.contiguous().view(torch.int8))
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
