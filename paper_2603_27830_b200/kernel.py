@@ -20,7 +20,7 @@ from typing import Any
 import numpy as np
 import torch
 
-from . import _device
+from . import _device, _hostmem
 from .gravity import WGS72, GravityModel
 from .tle import ELEMENT_COLUMNS, MeanElements
 
@@ -179,16 +179,17 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
     dev, sat_shape = _device_of(init)
     out_shape = np.broadcast_shapes(sat_shape, t.shape)
     p = int(np.prod(out_shape, dtype=np.int64))
-    r = np.empty(out_shape + (3,), dtype=dtype)
-    v = np.empty(out_shape + (3,), dtype=dtype)
     if p == 0:
-        return StateVector(r=r, v=v, error_code=np.zeros(out_shape, dtype=np.int32))
+        return StateVector(r=np.empty(out_shape + (3,), dtype=dtype),
+                           v=np.empty(out_shape + (3,), dtype=dtype),
+                           error_code=np.zeros(out_shape, dtype=np.int32))
     device = dev.device
     nd = len(out_shape)
     sat_p = (1,) * (nd - len(sat_shape)) + tuple(sat_shape)
     t_p = (1,) * (nd - t.ndim) + tuple(t.shape)
     sat_axes = [k for k in range(nd) if sat_p[k] > 1]
     t_axes = [k for k in range(nd) if t_p[k] > 1]
+    dt = _device.torch_dtype(dev.precision)
     with torch.cuda.device(device):
         if not set(sat_axes) & set(t_axes):
             # Cartesian product (e.g. init (n, 1) x times (m,)): one dense grid
@@ -199,30 +200,47 @@ def sgp4_propagate(init: SatInit, tsince_min) -> StateVector:
             rows = np.ascontiguousarray(sats.transpose(perm).reshape(n_sel, m_sel, -1)[:, 0, 0])
             tsel = np.ascontiguousarray(
                 np.broadcast_to(t, out_shape).transpose(perm).reshape(n_sel, m_sel, -1)[0, :, 0])
-            grid = _grid_of_rows(dev, rows, tsel)
-            planes = grid[0].cpu().numpy()
-            codes = grid[1].cpu().numpy()
+            planes, codes = _grid_of_rows(dev, rows, tsel)
+            # (3, n_sel, m_sel) -> out_shape + (3,) on the device, then one D2H each
             shape_p = tuple(out_shape[k] for k in perm)
-            inv = np.argsort(perm)
-            for dst, lo in ((r, 0), (v, 3)):
-                blk = planes[lo:lo + 3].reshape((3,) + shape_p)
-                dst[...] = np.moveaxis(blk.transpose([0] + [1 + a for a in inv]), 0, -1)
-            return StateVector(r=r, v=v,
-                               error_code=codes.reshape(shape_p).transpose(inv).copy())
-        # general broadcast: one (satellite, time) pair per cell
-        idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape),
-                              out_shape).ravel()
-        tt = np.array(np.broadcast_to(t, out_shape).ravel())          # writable copy
-        idx_d = torch.from_numpy(np.array(idx)).to(device)
-        t_d = torch.from_numpy(tt).to(device)
-        rv = torch.empty((6, p), dtype=_device.torch_dtype(dev.precision), device=device)
-        codes = torch.empty((p,), dtype=torch.int32, device=device)
-        _device.propagate_pairs(dev, idx_d, t_d, rv, codes, t_absmax=_device.times_absmax(tt))
-        rv_h = rv.cpu().numpy()
-        codes_h = codes.cpu().numpy()
-    r[...] = rv_h[:3].T.reshape(out_shape + (3,))
-    v[...] = rv_h[3:].T.reshape(out_shape + (3,))
-    return StateVector(r=r, v=v, error_code=codes_h.reshape(out_shape))
+            inv = [int(a) for a in np.argsort(perm)]
+            order = [1 + a for a in inv] + [0]
+
+            def arrange(blk):
+                return blk.reshape((3,) + shape_p).permute(order).contiguous()
+            r_d = arrange(planes[0:3])
+            v_d = arrange(planes[3:6])
+            c_d = codes.reshape(shape_p).permute(inv).contiguous()
+        else:
+            # general broadcast: one (satellite, time) pair per cell
+            if tuple(sat_p) == tuple(out_shape):
+                # every cell its own satellite, in order: no index array to upload
+                idx_d = torch.arange(p, dtype=torch.int64, device=device)
+            else:
+                idx = np.broadcast_to(np.arange(dev.n, dtype=np.int64).reshape(sat_shape),
+                                      out_shape).ravel()
+                idx_d = torch.from_numpy(np.ascontiguousarray(idx)).to(device)
+            tt = np.array(np.broadcast_to(t, out_shape).ravel())          # writable copy
+            t_d = torch.from_numpy(tt).to(device)
+            rv = torch.empty((6, p), dtype=dt, device=device)
+            c_d = torch.empty((p,), dtype=torch.int32, device=device)
+            _device.propagate_pairs(dev, idx_d, t_d, rv, c_d, t_absmax=_device.times_absmax(tt))
+            r_d = rv[0:3].t().contiguous()
+            v_d = rv[3:6].t().contiguous()
+        # one page-locked block for r, v and the codes (pooled, see _hostmem);
+        # pageable arrays when the result is larger than the pool keeps
+        specs = [(out_shape + (3,), dtype), (out_shape + (3,), dtype), (out_shape, np.int32)]
+        nbytes = 2 * r_d.numel() * r_d.element_size() + 4 * p
+        if nbytes <= _hostmem.cache_limit():
+            r, v, codes_h = _hostmem.empty(specs)
+            for dst, src in ((r, r_d), (v, v_d), (codes_h, c_d)):
+                torch.from_numpy(dst).view(-1).copy_(src.view(-1), non_blocking=True)
+            torch.cuda.current_stream(device).synchronize()
+        else:
+            r = r_d.cpu().numpy().reshape(out_shape + (3,))
+            v = v_d.cpu().numpy().reshape(out_shape + (3,))
+            codes_h = c_d.cpu().numpy().reshape(out_shape)
+    return StateVector(r=r, v=v, error_code=codes_h)
 
 
 def _grid_of_rows(dev, rows: np.ndarray, times: np.ndarray):
