@@ -50,6 +50,9 @@
 #ifndef SGP4B_SHFL_REC
 #define SGP4B_SHFL_REC 0          // fp32 records spread over the warp (shfl at use)
 #endif
+#ifndef SGP4B_SEC64
+#define SGP4B_SEC64 0             // fp32 secular angle on the FP64 pipe (see secular_angle64)
+#endif
 #ifndef SGP4B_K2_SERIES
 #define SGP4B_K2_SERIES 1           // class-2 (e < 0.1) series for 1/pl_lp, 1/den, 1/(1+betal)
 #endif
@@ -958,6 +961,31 @@ __device__ __forceinline__ VN<N> secular_angle(float x0, float rate, float rate_
   return r + (e + x0);
 }
 
+// The same angle on the FP64 pipe (SGP4B_SEC64): u = U0 + (UDOT_hi +
+// UDOT_lo) t in fp64 (t, U0 exact in fp64), reduced by k = rint(u / 2pi)
+// with one fma (|u| < 2^20 rad), rounded to fp32 once.  Moves the 9 FP32
+// ops of the double-float form to the otherwise idle FP64 pipe, at the cost
+// of two conversions per cell.
+template <bool LO, int N>
+__device__ __forceinline__ VN<N> secular_angle64(float x0, double rate, VN<N> t, VN<N> tl) {
+  VN<N> out;
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    double t0 = (double)t.h[i].x, t1 = (double)t.h[i].y;
+    if constexpr (LO) {
+      t0 += (double)tl.h[i].x;
+      t1 += (double)tl.h[i].y;
+    }
+    const double u0 = fma(rate, t0, (double)x0);
+    const double u1 = fma(rate, t1, (double)x0);
+    const double k0 = fma(u0, 0.15915494309189535, 6755399441055744.0) - 6755399441055744.0;
+    const double k1 = fma(u1, 0.15915494309189535, 6755399441055744.0) - 6755399441055744.0;
+    out.h[i] = make_float2((float)fma(-k0, 6.283185307179586, u0),
+                           (float)fma(-k1, 6.283185307179586, u1));
+  }
+  return out;
+}
+
 // (sin, cos)(a + d) from (sin, cos)(a) for |d| < 4e-3 (the J2 short-period
 // corrections and the last Newton step): d^3/6 < 1.1e-8 is below fp32
 // resolution, so sin d = d, cos d = 1 - d^2/2.
@@ -988,7 +1016,12 @@ __device__ __forceinline__ void cellv(const RT& R, VN<NC> t, VN<NC> tl, const Gr
   const V2 argpdf = fma2(t, R[P_ARGPDOT], sp<NC>(R[P_ARGPO]));
   const V2 t2 = t * t;
   const V2 nodem = fma2(t2, R[P_NODECF], fma2(t, R[P_NODEDOT], sp<NC>(R[P_NODEO])));
+#if SGP4B_SEC64
+  const V2 ubase = secular_angle64<LO, NC>(R[P_U0], (double)R[P_UDOT] + (double)R[P_UDOT_LO],
+                                           t, tl);
+#else
   const V2 ubase = secular_angle<LO, NC>(R[P_U0], R[P_UDOT], R[P_UDOT_LO], t, tl);
+#endif
 
   // drag  kernel.py:371-391.  With s = sqrt((xke/no)^(2/3)) folded in,
   // sqrt(am) = s tempa is one Horner polynomial in t; no templ is another.
