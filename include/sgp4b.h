@@ -114,6 +114,22 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
                       int64_t n, int64_t m, double* dr_dev, double* dv_dev,
                       void* stream);
 
+/* TLE catalogue ingest on the device: the columns of
+ * parse_catalog_columns (tle.py:390-433 here; the reference's per-record
+ * parse_tle + _canonical_elements, tle.py:185-276) for n records whose line
+ * 1 / line 2 start at byte offsets line1_dev[i] / line2_dev[i] of text_dev
+ * (size bytes; a line ends at '\n').
+ *   pow10_dev : 42 doubles: 10.0**k for k = 0..22 (exact), then the
+ *               host's 10.0**e for e = -9..9 (the B* exponent multiplier)
+ *   cols_dev  : (7, n) fp64 out, ELEMENT_COLUMNS order (init input)
+ *   status_dev: (n) int32 out, 0 or a bit per field whose text falls
+ *               outside the simple decimal syntax: the caller re-decodes
+ *               those records on the host. */
+int sgp4b_tle_columns(const uint8_t* text_dev, int64_t size,
+                      const int64_t* line1_dev, const int64_t* line2_dev,
+                      int64_t n, const double* pow10_dev, double* cols_dev,
+                      int32_t* status_dev, void* stream);
+
 /* Row summary of a code plane: flags_dev[i] = 1 when row i (codes_dev +
  * i*code_stride, m entries) holds a nonzero code, else 0.  Lets the host
  * copy of a BatchResult (batch.py:177-183, the int32 error plane) move only

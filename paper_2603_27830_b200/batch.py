@@ -137,6 +137,18 @@ def init_batch(elements: Sequence[MeanElements], grav: GravityModel = WGS72,
     (e.g. from :func:`~paper_2603_27830_b200.tle.parse_catalog_columns`).
     Never raises on bad elements: codes land in ``.error_codes``.
     """
+    if isinstance(elements, torch.Tensor):
+        # (7, n) columns already on a GPU (e.g. ingest.read_catalog_columns)
+        if elements.dim() != 2 or elements.shape[0] != 7:
+            raise ValueError("element columns must have shape (7, n)")
+        if elements.shape[1] == 0:
+            raise ValueError("empty element list")
+        if not elements.is_cuda:
+            elements = elements.numpy()
+        else:
+            el = elements.to(torch.float64).contiguous()
+            dev = _device.init_device_tensor(el, grav, _precision(precision), device)
+            return SatBatch(device_satrec=dev)
     if isinstance(elements, np.ndarray):
         cols = np.asarray(elements, dtype=np.float64)
         if cols.ndim != 2 or cols.shape[0] != 7:

@@ -2332,6 +2332,164 @@ __global__ void kepler_kernel(const T* __restrict__ axnl, const T* __restrict__ 
 
 // |r32 - r64| and |v32 - v64| per cell in fp64 where both codes are 0,
 // +inf elsewhere (so a per-column sort puts excluded cells last).
+// ======================================================================
+// TLE catalogue ingest (tle.py parse_catalog_columns, on the device)
+// ======================================================================
+// One thread per record: line 1 and line 2 start at byte offsets l1[i],
+// l2[i] of the catalogue text and end at the next '\n' (trailing '\r' and
+// spaces stripped, then space-padded to 69 columns, as
+// s.rstrip("\r\n ").ljust(69)[:69]).  Fields are decoded exactly as the
+// NumPy path does: a decimal field's value m / 10^k (m < 2^53, k <= 22) is
+// one correctly rounded IEEE division, which is what numpy's correctly
+// rounded string -> float64 cast returns; the implied-exponent B* field is
+// float("[-]0.digits") * 10.0**e (two roundings, like the host); then the
+// canonical conversion in the host's operation order.  A field outside the
+// simple syntax sets a bit in status[i]; the caller re-decodes those
+// records on the host, so every column equals parse_catalog_columns.
+struct TleLine {
+  const uint8_t* p;
+  int len;                          // columns before the stripped end
+  bool ascii;                       // byte columns == the host's str columns
+  __device__ __forceinline__ uint8_t at(int c) const { return c < len ? p[c] : (uint8_t)' '; }
+};
+
+__device__ __forceinline__ TleLine tle_line(const uint8_t* text, int64_t size, int64_t off) {
+  TleLine l;
+  l.p = text + off;
+  int n = 0;
+  bool ascii = true;
+  while (n < 80 && off + n < size && l.p[n] != '\n') {
+    ascii = ascii && l.p[n] < 0x80;
+    ++n;
+  }
+  while (n > 0 && (l.p[n - 1] == ' ' || l.p[n - 1] == '\r')) --n;
+  l.len = n < 69 ? n : 69;
+  l.ascii = ascii;
+  return l;
+}
+
+// columns [a, b) stripped of spaces -> [s, e); false if another whitespace
+// character is present (the host strip() would remove it too: host path)
+__device__ __forceinline__ bool tle_strip(const TleLine& l, int a, int b, int& s, int& e) {
+  s = a;
+  e = b;
+  while (s < e && l.at(s) == ' ') ++s;
+  while (e > s && l.at(e - 1) == ' ') --e;
+  for (int c = s; c < e; ++c) {
+    const uint8_t ch = l.at(c);
+    if (ch == '\t' || ch == '\r' || ch == '\n' || ch == '\v' || ch == '\f') return false;
+  }
+  return true;
+}
+
+// decimal "[+-]digits[.digits]" (at least one digit) -> correctly rounded
+// double; an empty field is +0.0 (as_float maps b"" to b"0")
+__device__ __forceinline__ bool tle_decimal(const TleLine& l, int a, int b, const double* pow10,
+                                            double& out) {
+  int s, e;
+  if (!tle_strip(l, a, b, s, e)) return false;
+  if (s == e) {
+    out = 0.0;
+    return true;
+  }
+  bool neg = false;
+  if (l.at(s) == '+' || l.at(s) == '-') {
+    neg = l.at(s) == '-';
+    ++s;
+  }
+  unsigned long long m = 0;
+  int digits = 0, frac = -1;
+  for (int c = s; c < e; ++c) {
+    const uint8_t ch = l.at(c);
+    if (ch == '.') {
+      if (frac >= 0) return false;
+      frac = 0;
+      continue;
+    }
+    if (ch < '0' || ch > '9') return false;
+    m = m * 10 + (ch - '0');
+    ++digits;
+    if (frac >= 0) ++frac;
+  }
+  if (digits == 0 || digits > 15) return false;     // m < 10^15 < 2^53: exact
+  const int k = frac < 0 ? 0 : frac;
+  const double v = k == 0 ? (double)m : __ddiv_rn((double)m, pow10[k]);
+  out = neg ? -v : v;
+  return true;
+}
+
+__global__ void tle_columns_kernel(const uint8_t* __restrict__ text, int64_t size,
+                                   const int64_t* __restrict__ l1, const int64_t* __restrict__ l2,
+                                   int64_t n, const double* __restrict__ pow10,
+                                   double* __restrict__ cols, int32_t* __restrict__ status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const TleLine a = tle_line(text, size, l1[i]);
+  const TleLine b = tle_line(text, size, l2[i]);
+  // a multi-byte UTF-8 character shifts the host's str columns: host path
+  int bad = (a.ascii && b.ascii) ? 0 : 128;
+  double revday = 0, incl = 0, raan = 0, argp = 0, ma = 0, ecc = 0, bstar = 0;
+  // line 2 fields (tle.py _L2)
+  if (!tle_decimal(b, 52, 63, pow10, revday)) bad |= 1;
+  if (!tle_decimal(b, 8, 16, pow10, incl)) bad |= 2;
+  if (!tle_decimal(b, 17, 25, pow10, raan)) bad |= 4;
+  if (!tle_decimal(b, 34, 42, pow10, argp)) bad |= 8;
+  if (!tle_decimal(b, 43, 51, pow10, ma)) bad |= 16;
+  {
+    // eccentricity: "0." + zfill(digits, 7); empty -> "0"
+    int s, e;
+    if (!tle_strip(b, 26, 33, s, e)) {
+      bad |= 32;
+    } else {
+      unsigned long long m = 0;
+      for (int c = s; c < e; ++c) {
+        const uint8_t ch = b.at(c);
+        if (ch < '0' || ch > '9') bad |= 32;
+        m = m * 10 + (ch - '0');
+      }
+      ecc = __ddiv_rn((double)m, pow10[7]);
+    }
+  }
+  {
+    // B*: "[sign]digits[sign digit]" (tle.py _implied_exponent_columns)
+    int s, e;
+    if (!tle_strip(a, 53, 61, s, e)) {
+      bad |= 64;
+    } else if (s < e) {
+      const int len = e - s;
+      const uint8_t first = a.at(s), last = a.at(e - 1), pen = len >= 2 ? a.at(e - 2) : 0;
+      const bool neg = first == '-';
+      const int start = s + ((first == '-' || first == '+') ? 1 : 0);
+      const bool has_exp = len >= 2 && (pen == '-' || pen == '+') && last >= '0' && last <= '9';
+      const int stop = has_exp ? e - 2 : e;
+      unsigned long long m = 0;
+      if (stop <= start || stop - start > 15) bad |= 64;
+      for (int c = start; c < stop; ++c) {
+        const uint8_t ch = a.at(c);
+        if (ch < '0' || ch > '9') bad |= 64;
+        m = m * 10 + (ch - '0');
+      }
+      if (!(bad & 64)) {
+        double v = __ddiv_rn((double)m, pow10[stop - start]);
+        v = neg ? -v : v;
+        // 10.0**e for e = -9..9 follow the 23 exact powers (the host's values)
+        if (has_exp) v = __dmul_rn(v, pow10[32 + (pen == '-' ? -(int)(last - '0') : (int)(last - '0'))]);
+        bstar = v;
+      }
+    }
+  }
+  // canonical columns (tle.py parse_catalog_columns), host operation order
+  const double deg = 0.017453292519943295;          // math.pi / 180.0
+  cols[0 * n + i] = __ddiv_rn(__dmul_rn(revday, kTwoPi), 1440.0);
+  cols[1 * n + i] = ecc;
+  cols[2 * n + i] = __dmul_rn(incl, deg);
+  cols[3 * n + i] = pymod_2pi(__dmul_rn(raan, deg));
+  cols[4 * n + i] = pymod_2pi(__dmul_rn(argp, deg));
+  cols[5 * n + i] = pymod_2pi(__dmul_rn(ma, deg));
+  cols[6 * n + i] = bstar;
+  status[i] = bad;
+}
+
 __global__ void drift_norms_kernel(const float* __restrict__ p32, const double* __restrict__ p64,
                                    const int32_t* __restrict__ c32, const int32_t* __restrict__ c64,
                                    int64_t cells, double* __restrict__ dr, double* __restrict__ dv) {
@@ -2467,7 +2625,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 4; }
+int sgp4b_abi_version(void) { return 5; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -2561,6 +2719,17 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
   drift_norms_kernel<<<blocks_for(cells, 256), 256, 0, (cudaStream_t)stream>>>(
       planes32_dev, planes64_dev, codes32_dev, codes64_dev, cells, dr_dev, dv_dev);
   return check_launch("sgp4b_drift_norms");
+}
+
+int sgp4b_tle_columns(const uint8_t* text_dev, int64_t size, const int64_t* line1_dev,
+                      const int64_t* line2_dev, int64_t n, const double* pow10_dev,
+                      double* cols_dev, int32_t* status_dev, void* stream) {
+  if (n <= 0 || size <= 0) return fail(SGP4B_EINVAL, "sgp4b_tle_columns: empty catalogue");
+  if (!text_dev || !line1_dev || !line2_dev || !pow10_dev || !cols_dev || !status_dev)
+    return fail(SGP4B_EINVAL, "sgp4b_tle_columns: null pointer argument");
+  tle_columns_kernel<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      text_dev, size, line1_dev, line2_dev, n, pow10_dev, cols_dev, status_dev);
+  return check_launch("sgp4b_tle_columns");
 }
 
 int sgp4b_code_rows(const int32_t* codes_dev, int64_t n, int64_t m, int64_t code_stride,
