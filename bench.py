@@ -454,9 +454,15 @@ def run_ours(args, world, rank, local) -> None:
     # planes AND int32 code plane cross PCIe every step (nothing is deferred
     # to a lazily mapped page), and the step reads a result value on the host
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    host_times = times.copy()
+    # the step's inputs live in pinned host memory (element columns, times)
+    from paper_2603_27830_b200 import _hostmem
+    host_cols, host_times = _hostmem.empty(
+        [(cols.shape, np.float64), (times.shape, np.float32 if precision == 32 else np.float64)])
+    host_cols[...] = cols
+    host_times[...] = times
+    cols_in = host_cols
     for _ in range(2):
-        res = propagate_batch(init_batch(cols, precision=precision, device=device), host_times)
+        res = propagate_batch(init_batch(cols_in, precision=precision, device=device), host_times)
         del res
     torch.cuda.synchronize()
     if world > 1:
@@ -465,7 +471,7 @@ def run_ours(args, world, rank, local) -> None:
     res = None
     for _ in range(e2e_steps):
         del res
-        res = propagate_batch(init_batch(cols, precision=precision, device=device), host_times)
+        res = propagate_batch(init_batch(cols_in, precision=precision, device=device), host_times)
         checksum = int(res.error[-1, -1]) + int(res.error[0, 0])   # host reads of the result
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
@@ -519,7 +525,7 @@ def run_ours(args, world, rank, local) -> None:
                     "pcie_d2h_gbs_measured": d2h_gbs,
                     "pcie_frac": (h2d_bytes + d2h_bytes) / e2e_s / (d2h_gbs * 1e9),
                     "code_plane_bytes_zero_filled_on_host": zero_filled,
-                    "api": "propagate_batch(init_batch(host columns), host times) -> numpy "
+                    "api": "propagate_batch(init_batch(pinned host columns), pinned host times) -> numpy "
                            "planes + int32 codes in pinned host memory, every element written "
                            "inside the timed step: the planes and the code rows holding a "
                            "nonzero code cross PCIe, the other code rows are zero-filled on "

@@ -165,7 +165,12 @@ def init_batch(elements: Sequence[MeanElements], grav: GravityModel = WGS72,
 
 
 def _times(sats: SatBatch, times) -> np.ndarray:
-    t = np.array(times, dtype=sats.dtype)          # own, writable copy (M values)
+    # the caller's array when it already is a contiguous, writable vector of
+    # the batch dtype (e.g. in pinned memory: its H2D is then a plain DMA);
+    # otherwise a cast copy.  Every use completes before the call returns.
+    t = np.asarray(times, dtype=sats.dtype)
+    if not (t.flags.c_contiguous and t.flags.writeable):
+        t = np.array(t)
     if t.ndim != 1 or t.size == 0:
         raise ValueError("times must be a non-empty 1-D array")
     return t
