@@ -114,6 +114,18 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
                       int64_t n, int64_t m, double* dr_dev, double* dv_dev,
                       void* stream);
 
+/* Nearest-rank percentiles per column of the drift norms (drift.py:46-49,
+ * 74-92): for each column j, the rank-th smallest finite value of dr and of
+ * dv with rank = max(1, ceil(count_j * pct_frac[k])), k = 0..2.
+ *   pct_frac  : HOST pointer to 3 doubles (p / 100.0, e.g. 0.05, 0.5, 0.95)
+ *   table_dev : (6, m) fp64 out: dr at the 3 fractions, then dv; NaN for a
+ *               column without finite values
+ *   counts_dev: (m) int64 out, finite cells per column */
+int sgp4b_drift_percentiles(const double* dr_dev, const double* dv_dev,
+                            int64_t n, int64_t m, const double* pct_frac,
+                            double* table_dev, int64_t* counts_dev,
+                            void* stream);
+
 /* TLE catalogue ingest on the device: the columns of
  * parse_catalog_columns (tle.py:390-433 here; the reference's per-record
  * parse_tle + _canonical_elements, tle.py:185-276) for n records whose line

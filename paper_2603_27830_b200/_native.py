@@ -16,7 +16,7 @@ LIB_PATH = _HERE / LIB_NAME
 
 SATREC_FIELDS = 33
 RECORD_SLOTS = 40
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 #: every symbol include/sgp4b.h declares, in header order
 EXPORTED_SYMBOLS = (
@@ -25,6 +25,7 @@ EXPORTED_SYMBOLS = (
     "sgp4b_propagate_grid",
     "sgp4b_propagate_pairs",
     "sgp4b_drift_norms",
+    "sgp4b_drift_percentiles",
     "sgp4b_tle_columns",
     "sgp4b_code_rows",
     "sgp4b_solve_kepler",
@@ -46,6 +47,7 @@ _SIGNATURES = {
     "sgp4b_propagate_pairs": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, ctypes.c_double, _c_int,
                                        _vp, _vp, _vp, _vp]),
     "sgp4b_drift_norms": (_c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
+    "sgp4b_drift_percentiles": (_c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp, _vp]),
     "sgp4b_tle_columns": (_c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp]),
     "sgp4b_code_rows": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp]),
     "sgp4b_solve_kepler": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _vp, _vp]),

@@ -2543,6 +2543,87 @@ __global__ void __launch_bounds__(256) code_rows_kernel(const int32_t* __restric
   }
 }
 
+// Per-column nearest-rank percentiles of the drift norms (drift.py:46-49:
+// rank = max(1, ceil(count * p / 100)) among the finite values of a column,
+// the rank-th smallest).  One block per column; each of the six selections
+// (p5/p50/p95 of |dr| and |dv|) is an MSB-first radix select over the
+// values' bit patterns (non-negative doubles order as unsigned integers;
+// +inf marks excluded cells and sorts after every finite value), 8 bits per
+// pass.  Exact: the result is the element a full column sort would place at
+// that rank.
+struct Pct3 {
+  double f[3];                      // p / 100.0 as the host computes it
+};
+
+__global__ void __launch_bounds__(256) drift_pct_kernel(const double* __restrict__ dr,
+                                                        const double* __restrict__ dv, int64_t n,
+                                                        int64_t m, Pct3 pct,
+                                                        double* __restrict__ table,
+                                                        int64_t* __restrict__ counts) {
+  __shared__ unsigned hist[6][256];
+  __shared__ unsigned long long prefix[6];
+  __shared__ long long rank[6];
+  __shared__ unsigned long long cnt_s[2];
+  const int64_t j = blockIdx.x;
+  const int tid = threadIdx.x;
+  // finite counts of the column (excluded cells are +inf)
+  unsigned long long cr = 0, cv = 0;
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    cr += isfinite(__ldg(dr + i * m + j)) ? 1 : 0;
+    cv += isfinite(__ldg(dv + i * m + j)) ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+    cv += __shfl_xor_sync(0xffffffffu, cv, o);
+  }
+  if (tid < 2) cnt_s[tid] = 0;
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    atomicAdd(&cnt_s[0], cr);
+    atomicAdd(&cnt_s[1], cv);
+  }
+  __syncthreads();
+  if (tid < 6) {
+    const unsigned long long c = cnt_s[tid / 3];
+    long long r = (long long)ceil((double)c * pct.f[tid % 3]);
+    rank[tid] = r < 1 ? 1 : r;
+    prefix[tid] = 0;
+  }
+  if (tid == 0) counts[j] = (int64_t)cnt_s[0];
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int k = tid; k < 6 * 256; k += blockDim.x) (&hist[0][0])[k] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const unsigned long long xr = (unsigned long long)__double_as_longlong(__ldg(dr + i * m + j));
+      const unsigned long long xv = (unsigned long long)__double_as_longlong(__ldg(dv + i * m + j));
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const unsigned long long x = s < 3 ? xr : xv;
+        const bool match = pass == 0 || ((x ^ prefix[s]) >> (shift + 8)) == 0;
+        if (match) atomicAdd(&hist[s][(x >> shift) & 255], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < 6) {
+      long long r = rank[tid];
+      int b = 0;
+      for (; b < 255; ++b) {
+        if (r <= (long long)hist[tid][b]) break;
+        r -= hist[tid][b];
+      }
+      rank[tid] = r;
+      prefix[tid] |= (unsigned long long)b << shift;
+    }
+    __syncthreads();
+  }
+  if (tid < 6) {
+    const unsigned long long c = cnt_s[tid / 3];
+    table[tid * m + j] = c > 0 ? __longlong_as_double((long long)prefix[tid]) : CUDART_NAN;
+  }
+}
+
 bool grav_from(const double* grav, Grav& g) {
   if (grav == nullptr) return false;
   g.mu = grav[0]; g.re = grav[1]; g.xke = grav[2]; g.tumin = grav[3];
@@ -2625,7 +2706,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 5; }
+int sgp4b_abi_version(void) { return 6; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -2719,6 +2800,20 @@ int sgp4b_drift_norms(const float* planes32_dev, const double* planes64_dev,
   drift_norms_kernel<<<blocks_for(cells, 256), 256, 0, (cudaStream_t)stream>>>(
       planes32_dev, planes64_dev, codes32_dev, codes64_dev, cells, dr_dev, dv_dev);
   return check_launch("sgp4b_drift_norms");
+}
+
+int sgp4b_drift_percentiles(const double* dr_dev, const double* dv_dev, int64_t n, int64_t m,
+                            const double* pct_frac, double* table_dev, int64_t* counts_dev,
+                            void* stream) {
+  if (n <= 0 || m <= 0) return fail(SGP4B_EINVAL, "sgp4b_drift_percentiles: empty grid");
+  if (!dr_dev || !dv_dev || !pct_frac || !table_dev || !counts_dev)
+    return fail(SGP4B_EINVAL, "sgp4b_drift_percentiles: null pointer argument");
+  if (m > 0x7fffffff) return fail(SGP4B_EINVAL, "sgp4b_drift_percentiles: too many columns");
+  Pct3 pct;
+  for (int k = 0; k < 3; ++k) pct.f[k] = pct_frac[k];
+  drift_pct_kernel<<<(unsigned)m, 256, 0, (cudaStream_t)stream>>>(dr_dev, dv_dev, n, m, pct,
+                                                                   table_dev, counts_dev);
+  return check_launch("sgp4b_drift_percentiles");
 }
 
 int sgp4b_tle_columns(const uint8_t* text_dev, int64_t size, const int64_t* line1_dev,

@@ -14,9 +14,9 @@ The machinery is pinned separately: ``drift_from_grids`` takes ANY pair of
 fp32/fp64 grids (e.g. the reference's own, via the oracle in the tests) and
 reproduces the reference's ``drift_report`` table bit for bit
 (tests/golden/ref_drift.npz).  Norms come from the ``sgp4b_drift_norms``
-kernel (NumPy's rounding order), the percentiles from a per-column sort on
-the device with excluded cells last as +inf; only the (6, M) table crosses
-to the host.
+kernel (NumPy's rounding order), the percentiles from a per-column radix
+select on the device (``sgp4b_drift_percentiles``, excluded cells are +inf);
+only the (6, M) table crosses to the host.
 """
 
 from __future__ import annotations
@@ -65,15 +65,6 @@ def _nearest_rank(sorted_values: np.ndarray, pct: float) -> float:
     return float(sorted_values[rank - 1])
 
 
-def _nearest_rank_columns(sorted_vals: torch.Tensor, counts: torch.Tensor, pct: float) -> torch.Tensor:
-    """Nearest-rank percentile per column of a column-sorted (n, m) tensor
-    whose first counts[j] entries of column j are valid (drift.py:46-49)."""
-    rank = torch.clamp(torch.ceil(counts.double() * (pct / 100.0)).long(), min=1)
-    idx = (rank - 1).clamp(max=sorted_vals.shape[0] - 1)
-    vals = sorted_vals.gather(0, idx.unsqueeze(0)).squeeze(0)
-    return torch.where(counts > 0, vals, torch.full_like(vals, float("nan")))
-
-
 def drift_report(tles, horizon_days: float, step_minutes: float,
                  grav: GravityModel = WGS72) -> PrecisionReport:
     """Propagate the corpus at 32 and 64 bit and report drift percentiles
@@ -117,14 +108,18 @@ def drift_from_grids(lo, hi, times, corpus_size: int | None = None,
             p32.data_ptr(), p64.data_ptr(), c32.data_ptr(), c64.data_ptr(), n, m,
             dr.data_ptr(), dv.data_ptr(),
             torch.cuda.current_stream(device).cuda_stream))
-        counts = torch.isfinite(dr).sum(dim=0)
+        # per-column nearest-rank selection on the device (radix select,
+        # exact: the element a full column sort would put at the rank)
+        table_d = torch.empty((6, m), dtype=torch.float64, device=device)
+        counts = torch.empty((m,), dtype=torch.int64, device=device)
+        frac = np.array([p / 100.0 for p in (5, 50, 95)], dtype=np.float64)
+        _native.check(_native.load().sgp4b_drift_percentiles(
+            dr.data_ptr(), dv.data_ptr(), n, m, frac.ctypes.data, table_d.data_ptr(),
+            counts.data_ptr(), torch.cuda.current_stream(device).cuda_stream))
         included = int(counts.sum())
         if included == 0:
             raise EmptyReportError("all corpus cells carry nonzero error codes")
-        dr_s = torch.sort(dr, dim=0).values
-        dv_s = torch.sort(dv, dim=0).values
-        table = torch.stack([_nearest_rank_columns(x, counts, p)
-                             for x in (dr_s, dv_s) for p in (5, 50, 95)]).cpu().numpy()
+        table = table_d.cpu().numpy()
     days = np.asarray(times, dtype=np.float64) / 1440.0
     return PrecisionReport(
         days=days, p5_km=table[0], p50_km=table[1], p95_km=table[2],

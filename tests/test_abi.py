@@ -62,6 +62,8 @@ GRAV = np.zeros(8)
                                      (1 << 31), (1 << 31), 1, (1 << 31), None),  # m > 2^30
     lambda L: L.sgp4b_propagate_pairs(1, 1, 1, None, 0, 1.0, 64, GRAV.ctypes.data, 1, 1, None),
     lambda L: L.sgp4b_solve_kepler(1, 1, 1, 4, 8, 1, None),
+    lambda L: L.sgp4b_drift_percentiles(1, 1, 0, 4, 1, 1, 1, None),            # n = 0
+    lambda L: L.sgp4b_drift_percentiles(1, None, 4, 4, 1, 1, 1, None),         # null
     lambda L: L.sgp4b_tle_columns(1, 100, 1, 1, 0, 1, 1, 1, None),              # n = 0
     lambda L: L.sgp4b_tle_columns(None, 100, 1, 1, 4, 1, 1, 1, None),           # null
     lambda L: L.sgp4b_code_rows(1, 0, 4, 4, 1, None),                           # n = 0

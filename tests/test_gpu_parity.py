@@ -792,6 +792,41 @@ def test_long_rows_split_into_column_blocks(corpus_columns, precision, monkeypat
                        split.planes.contiguous().view(torch.int8))
 
 
+@pytest.mark.parametrize("n,m", [(1, 3), (7, 5), (1000, 17), (50_000, 4)])
+def test_drift_percentile_select_matches_sort(n, m):
+    """sgp4b_drift_percentiles (per-column radix select) returns exactly the
+    nearest-rank elements of a full column sort, with +inf cells excluded,
+    ties, subnormals and an all-excluded column (NaN)."""
+    import torch
+    from paper_2603_27830_b200 import _native
+    rng = np.random.default_rng(n + m)
+    dr = rng.lognormal(-6, 2, size=(n, m))
+    dv = rng.lognormal(-12, 3, size=(n, m))
+    dr[rng.random((n, m)) < 0.1] = np.inf
+    dv[rng.random((n, m)) < 0.1] = np.inf
+    dr[:, 0] = np.inf                                   # a column with no finite cell
+    if n > 3:
+        dr[: n // 2, 1] = 1e-310                        # ties, subnormal
+        dv[:, 2] = 0.0
+    frac = np.array([0.05, 0.5, 0.95])
+    table = torch.empty((6, m), dtype=torch.float64, device="cuda")
+    counts = torch.empty((m,), dtype=torch.int64, device="cuda")
+    d_r, d_v = torch.from_numpy(dr).cuda(), torch.from_numpy(dv).cuda()
+    _native.check(_native.load().sgp4b_drift_percentiles(
+        d_r.data_ptr(), d_v.data_ptr(), n, m, frac.ctypes.data, table.data_ptr(),
+        counts.data_ptr(), None))
+    got = table.cpu().numpy()
+    for j in range(m):
+        assert counts[j].item() == int(np.isfinite(dr[:, j]).sum())
+        for q, x in enumerate((dr, dv)):
+            col = np.sort(x[:, j])
+            c = int(np.isfinite(x[:, j]).sum())
+            for k, f in enumerate(frac):
+                want = col[max(1, int(np.ceil(c * f))) - 1] if c else np.nan
+                g = got[3 * q + k, j]
+                assert (np.isnan(want) and np.isnan(g)) or g == want, (j, q, k, g, want)
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
