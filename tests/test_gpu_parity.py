@@ -864,6 +864,8 @@ def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     # same shape, no failing rows: the pooled block that held codes is reused
     n_prev = host.n
     del host
+    import gc
+    gc.collect()                  # the block goes back to the pool now
     clean = pkg.init_batch(corpus_columns[:, 100:100 + n_prev])
     reuses = _hostmem.stats()["reuses"]
     host = pkg.propagate_batch(clean, times)
