@@ -71,9 +71,10 @@ def _host_lines(data: np.ndarray) -> tuple[list[str], list[str]]:
 
 def _as_bytes(source) -> np.ndarray:
     if isinstance(source, np.ndarray):
-        return np.ascontiguousarray(source.reshape(-1).view(np.uint8))
+        arr = np.ascontiguousarray(source.reshape(-1).view(np.uint8))
+        return arr if arr.flags.writeable else arr.copy()
     if isinstance(source, (bytes, bytearray, memoryview)):
-        return np.frombuffer(bytes(source), dtype=np.uint8)
+        return np.frombuffer(bytearray(source), dtype=np.uint8)    # writable copy
     if isinstance(source, (str, os.PathLike)):
         return np.fromfile(source, dtype=np.uint8)
     raise TypeError("source must be a path, bytes or a uint8 array")
