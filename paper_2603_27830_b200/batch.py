@@ -430,6 +430,24 @@ def last_transfer() -> dict:
     return dict(_last_transfer)
 
 
+def flag_runs(flags: np.ndarray, max_runs: int) -> list[tuple[int, int]]:
+    """Half-open row ranges [a, b) covering the rows whose flag is set, in
+    order; the whole range [(0, n)] when there are more than ``max_runs``
+    runs or more than half the rows are flagged (one copy is then cheaper)."""
+    n = int(flags.shape[0])
+    rows = np.flatnonzero(flags)
+    if rows.size == 0:
+        return []
+    if rows.size * 2 > n:
+        return [(0, n)]
+    cut = np.flatnonzero(np.diff(rows) != 1) + 1
+    if cut.size + 1 > max_runs:
+        return [(0, n)]
+    starts = rows[np.r_[0, cut]]
+    ends = rows[np.r_[cut - 1, rows.size - 1]] + 1
+    return list(zip(starts.tolist(), ends.tolist()))
+
+
 class _CodesToHost:
     """D2H of an (n, m) int32 code plane that moves only the rows holding a
     nonzero code.  ``__init__`` (before the planes' D2H is queued) runs
@@ -459,15 +477,7 @@ class _CodesToHost:
     def finish(self) -> None:
         self.ready.synchronize()
         n = self.error_h.shape[0]
-        rows = np.flatnonzero(self.flags_h)
-        runs = []
-        if rows.size:
-            cut = np.flatnonzero(np.diff(rows) != 1) + 1
-            starts = rows[np.r_[0, cut]]
-            ends = rows[np.r_[cut - 1, rows.size - 1]] + 1
-            runs = list(zip(starts.tolist(), ends.tolist()))
-        if len(runs) > self.MAX_RUNS or rows.size * 2 > n:
-            runs = [(0, n)]
+        runs = flag_runs(self.flags_h, self.MAX_RUNS)
         row_bytes = self.error_h.strides[0]
         self.d2h_bytes = self.flags_h.nbytes + sum(b - a for a, b in runs) * row_bytes
         lo = 0

@@ -248,3 +248,39 @@ def test_pack_rejects_init_codes_the_record_cannot_hold():
     for bad in ([-1, 0], [0, 1 << 23]):
         with _pytest.raises(ValueError, match="error_code_at_init"):
             _device.pack_device(sr, np.array(bad), np.zeros(2, np.uint8), WGS72, 64)
+
+
+# ---- host logic of the transfer and ingest paths (no GPU) -----------------
+
+def test_flag_runs():
+    from paper_2603_27830_b200.batch import flag_runs
+    f = np.zeros(20, np.uint8)
+    assert flag_runs(f, 64) == []
+    f[[2, 3, 4, 9, 19]] = 1
+    assert flag_runs(f, 64) == [(2, 5), (9, 10), (19, 20)]
+    assert flag_runs(f, 2) == [(0, 20)]                      # too many runs
+    g = np.ones(20, np.uint8)
+    g[:9] = 0
+    assert flag_runs(g, 64) == [(0, 20)]                     # more than half flagged
+    one = np.array([1], np.uint8)
+    assert flag_runs(one, 64) == [(0, 1)]
+
+
+def test_ingest_host_lines_follow_read_tle_file(tmp_path):
+    """The host path of read_catalog_columns pairs lines exactly as
+    read_tle_file does (universal newlines, blank and name lines skipped,
+    the same 'line 2 missing' error)."""
+    from paper_2603_27830_b200.ingest import _as_bytes, _host_lines
+    from paper_2603_27830_b200.tle import TleError, read_tle_file
+    a = "1 25544U 98067A   24001.50000000  .00016717  00000-0  10270-3 0  9990"
+    b = "2 25544  51.6416 247.4627 0006703 130.5360 325.0288 15.49815367 12345"
+    for text in (f"ISS\n{a}\n{b}\n", f"{a}\r\n{b}\r\n", f"\n\n{a}\n   \n{b}", f"{a}\r{b}\r",
+                 f"X\n{b}\n{a}\n{b}\n"):
+        path = tmp_path / "c.tle"
+        path.write_bytes(text.encode())
+        l1, l2 = _host_lines(_as_bytes(path))
+        recs = read_tle_file(path)
+        assert len(l1) == len(recs) == 1 and l1[0].rstrip() == a and l2[0].rstrip() == b
+    with pytest.raises(TleError, match="line 2 missing"):
+        _host_lines(_as_bytes(f"{a}\n{a}\n{b}\n".encode()))
+    assert _as_bytes(b"xy").flags.writeable
