@@ -155,6 +155,13 @@ int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev,
                        const void* u_dev, int64_t n, int precision,
                        void* out_dev, void* stream);
 
+/* Lets kernels running on `device` load and store `peer`'s memory (NVLink
+ * peer access), so a satellite shard computed on one GPU can store its rows
+ * straight into a grid that lives on another (no gather step).  0 when
+ * enabled (or already enabled, or device == peer), SGP4B_ECUDA when the
+ * pair cannot be peers. */
+int sgp4b_peer_access(int device, int peer);
+
 /* Page-locked (pinned, portable) host memory for result grids.  The
  * reference returns pageable np.empty grids (batch.py:177-183); results that
  * come back over PCIe need pinned memory for full-rate D2H, and the Python

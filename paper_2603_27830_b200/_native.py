@@ -16,7 +16,7 @@ LIB_PATH = _HERE / LIB_NAME
 
 SATREC_FIELDS = 33
 RECORD_SLOTS = 40
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 #: every symbol include/sgp4b.h declares, in header order
 EXPORTED_SYMBOLS = (
@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = (
     "sgp4b_tle_columns",
     "sgp4b_code_rows",
     "sgp4b_solve_kepler",
+    "sgp4b_peer_access",
     "sgp4b_host_alloc",
     "sgp4b_host_free",
     "sgp4b_last_error",
@@ -51,6 +52,7 @@ _SIGNATURES = {
     "sgp4b_tle_columns": (_c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp]),
     "sgp4b_code_rows": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp]),
     "sgp4b_solve_kepler": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _vp, _vp]),
+    "sgp4b_peer_access": (_c_int, [_c_int, _c_int]),
     "sgp4b_host_alloc": (_c_int, [_c_i64, ctypes.POINTER(_vp)]),
     "sgp4b_host_free": (_c_int, [_vp]),
     "sgp4b_last_error": (ctypes.c_char_p, []),

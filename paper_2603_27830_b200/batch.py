@@ -19,7 +19,7 @@ from typing import Any, Callable, Sequence
 import numpy as np
 import torch
 
-from . import _device, _hostmem
+from . import _device, _hostmem, _native
 from .gravity import WGS72, GravityModel
 from .kernel import SatInit, satinit_from_device, _device_of
 from .tle import MeanElements, elements_to_columns
@@ -199,7 +199,8 @@ def _alloc_grid(n: int, m: int, precision: int, device, pin: bool = False):
 
 
 def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
-                           times_lo=None, t_absmax: float | None = None) -> BatchResult:
+                           times_lo=None, t_absmax: float | None = None,
+                           devices=None) -> BatchResult:
     """Propagate every satellite to every time, leaving the grid in HBM.
 
     ``times`` is a 1-D array/tensor (cast to the batch dtype); ``out`` may
@@ -207,8 +208,14 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
     (fp32 batches only) carries the low words of fp64 times for the
     double-float secular stage.  ``t_absmax`` may give max |times| when the
     caller knows it (device-tensor times are otherwise reduced on the device,
-    one sync).  Returns a BatchResult of torch tensors.
+    one sync).  ``devices`` spreads the satellites over several GPUs of this
+    process; the grid still lands on the batch's device (see
+    :func:`_propagate_device_multi`).  Returns a BatchResult of torch tensors.
     """
+    if devices is not None and len(list(devices)) > 0:
+        if times_lo is not None:
+            raise ValueError("times_lo is not supported with devices=")
+        return _propagate_device_multi(sats, times, out, t_absmax, devices)
     dev = sats.device_satrec
     with torch.cuda.device(dev.device):
         if isinstance(times, torch.Tensor):
@@ -232,6 +239,68 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
             planes, error = _check_out(out, sats.n, m, dev.precision, dev.device)
         _device.propagate_grid(dev, t_d, planes, error, times_lo=times_lo, t_absmax=t_absmax)
     return BatchResult(planes=planes, error=error, n=sats.n, m=m)
+
+
+def _propagate_device_multi(sats: SatBatch, times, out, t_absmax, devices) -> BatchResult:
+    """The grid on the batch's (home) device, computed by several GPUs: each
+    takes a balanced satellite range (``partition_work``'s rule), runs the
+    grid kernel on its own stream, and — with NVLink peer access — stores its
+    rows straight into the home device's grid (the kernel's output pointers
+    are the peer's memory: no separate gather).  Without peer access a
+    device computes into local memory and its rows are copied over.  Cells
+    are bitwise equal to the single-device grid."""
+    from .shard import shard_bounds
+    dev = sats.device_satrec
+    home = dev.device
+    devs = _devices(devices)
+    t = times.detach().cpu().numpy() if isinstance(times, torch.Tensor) else times
+    t = _times(sats, t)
+    n, m = sats.n, t.size
+    if t_absmax is None:
+        t_absmax = _device.times_absmax(t)
+    lib = _native.load()
+    with torch.cuda.device(home):
+        if out is None:
+            planes, error = _alloc_grid(n, m, dev.precision, home)
+        else:
+            planes, error = _check_out(out, n, m, dev.precision, home)
+        home_stream = torch.cuda.current_stream(home)
+        ready = torch.cuda.Event()
+        ready.record(home_stream)            # records and the output exist
+    jobs = []
+    for g, d in enumerate(devs):
+        lo, hi = shard_bounds(n, len(devs), g)
+        if hi <= lo:
+            continue
+        direct = d == home or lib.sgp4b_peer_access(d.index, home.index) == 0
+        with torch.cuda.device(d):
+            stream = torch.cuda.Stream(d)
+            stream.wait_event(ready)
+            with torch.cuda.stream(stream):
+                sub = _shard_satrec(dev, lo, hi, d)
+                t_d = torch.from_numpy(t).to(d, non_blocking=True)
+                if direct:
+                    # rows lo..hi of the home grid, written from device d
+                    _device.propagate_grid(sub, t_d, planes[:, lo:hi], error[lo:hi],
+                                           t_absmax=t_absmax)
+                    local = None
+                else:
+                    local = _alloc_grid(hi - lo, m, dev.precision, d)
+                    _device.propagate_grid(sub, t_d, local[0], local[1], t_absmax=t_absmax)
+                done = torch.cuda.Event()
+                done.record(stream)
+        jobs.append((d, stream, done, lo, hi, local, sub, t_d))
+    with torch.cuda.device(home):
+        for d, stream, done, lo, hi, local, *_ in jobs:
+            home_stream.wait_event(done)
+            if local is not None:
+                planes[:, lo:hi].copy_(local[0], non_blocking=True)
+                error[lo:hi].copy_(local[1], non_blocking=True)
+                for x in local:                  # read by the home stream
+                    x.record_stream(home_stream)
+    for _, stream, *_ in jobs:
+        stream.synchronize()                 # shard inputs/temporaries outlive their use
+    return BatchResult(planes=planes, error=error, n=n, m=m)
 
 
 def _check_out(out, n: int, m: int, precision: int, device):

@@ -2706,7 +2706,7 @@ inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + thre
 // ======================================================================
 extern "C" {
 
-int sgp4b_abi_version(void) { return 6; }
+int sgp4b_abi_version(void) { return 7; }
 
 #ifdef SGP4B_TIMELINE
 int sgp4b_debug_timeline(unsigned long long* host, int warps) {
@@ -2855,6 +2855,26 @@ int sgp4b_solve_kepler(const void* axnl_dev, const void* aynl_dev, const void* u
         static_cast<const float*>(axnl_dev), static_cast<const float*>(aynl_dev),
         static_cast<const float*>(u_dev), n, static_cast<float*>(out_dev));
   return check_launch("sgp4b_solve_kepler");
+}
+
+int sgp4b_peer_access(int device, int peer) {
+  if (device == peer) return SGP4B_OK;
+  int can = 0;
+  cudaError_t e = cudaDeviceCanAccessPeer(&can, device, peer);
+  if (e != cudaSuccess || !can) {
+    cudaGetLastError();
+    return fail(SGP4B_ECUDA, "sgp4b_peer_access: device %d cannot access device %d", device, peer);
+  }
+  int prev = -1;
+  cudaGetDevice(&prev);
+  e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+  cudaGetLastError();
+  if (prev >= 0) cudaSetDevice(prev);
+  if (e != cudaSuccess)
+    return fail(SGP4B_ECUDA, "sgp4b_peer_access(%d -> %d): %s", device, peer, cudaGetErrorString(e));
+  return SGP4B_OK;
 }
 
 int sgp4b_host_alloc(int64_t nbytes, void** out) {

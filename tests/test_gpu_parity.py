@@ -827,6 +827,37 @@ def test_drift_percentile_select_matches_sort(n, m):
                 assert (np.isnan(want) and np.isnan(g)) or g == want, (j, q, k, g, want)
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("ndev", [1, 2, 3])
+def test_device_grid_multi_device_bitwise(corpus_columns, failure_table, precision, ndev):
+    """propagate_batch_device(devices=...): each device stores its rows
+    straight into the home device's grid (peer memory on a multi-GPU box;
+    the same GPU named several times here) — bitwise equal to one launch,
+    also into a caller-provided `out`."""
+    import torch
+    pkg = _gpu()
+    bad = np.array([row["elements"] for row in failure_table["cases"].values()]).T
+    cols = np.concatenate([corpus_columns[:, :100], bad, corpus_columns[:, 100:157]], axis=1)
+    sats = pkg.init_batch(cols, precision=precision)
+    times = np.linspace(-60.0, 2880.0, 130)
+    one = pkg.propagate_batch_device(sats, times)
+    devs = [0] * ndev
+    multi = pkg.propagate_batch_device(sats, times, devices=devs)
+    torch.cuda.synchronize()
+    assert torch.equal(one.error, multi.error)
+    assert torch.equal(one.planes.contiguous().view(torch.int8),
+                       multi.planes.contiguous().view(torch.int8))
+    dt = torch.float32 if precision == 32 else torch.float64
+    out = (torch.empty((6, sats.n, 130), dtype=dt, device="cuda"),
+           torch.empty((sats.n, 130), dtype=torch.int32, device="cuda"))
+    res = pkg.propagate_batch_device(sats, times, out=out, devices=devs)
+    torch.cuda.synchronize()
+    assert res.planes.data_ptr() == out[0].data_ptr()
+    assert torch.equal(out[1], one.error)
+    from paper_2603_27830_b200 import _native
+    assert _native.load().sgp4b_peer_access(0, 0) == 0
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
