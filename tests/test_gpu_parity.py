@@ -858,6 +858,50 @@ def test_device_grid_multi_device_bitwise(corpus_columns, failure_table, precisi
     assert _native.load().sgp4b_peer_access(0, 0) == 0
 
 
+def _harsh_catalogue(rng, n):
+    """Every Kepler class (e up to 0.8), deep-space periods, a few perigees
+    below the surface, |B*| up to 1e-2 of both signs (tools/exp/parity_campaign.py)."""
+    xke = 0.07436691613317342
+    no = 2 * np.pi / rng.uniform(87.0, 240.0, n)
+    u = rng.random(n)
+    ecc = np.where(u < 0.4, rng.uniform(1e-5, 3e-3, n),
+          np.where(u < 0.7, rng.uniform(3e-3, 0.1, n),
+          np.where(u < 0.9, rng.uniform(0.1, 0.4, n), rng.uniform(0.4, 0.8, n))))
+    a = (xke / no) ** (2.0 / 3.0)
+    low = rng.random(n) < 0.05
+    ecc = np.where(~low & (a * (1 - ecc) < 1.02), np.maximum(0.0, 1 - 1.02 / a), ecc)
+    bstar = np.exp(rng.uniform(np.log(1e-6), np.log(1e-2), n)) * np.where(rng.random(n) < 0.1, -1, 1)
+    return np.stack([no, ecc, rng.uniform(0, np.pi, n), rng.uniform(0, 2 * np.pi, n),
+                     rng.uniform(0, 2 * np.pi, n), rng.uniform(0, 2 * np.pi, n), bstar])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_harsh_random_catalogues(oracle, seed):
+    """Randomized harsh catalogues over -2..+14 days: fp64 codes bit-exact
+    and within tolerance outside the degenerate-drag cells (tempa < 0.2 or
+    |em| > 0.5, where the reference itself is ill-conditioned: DESIGN §4);
+    fp32 codes equal the reference fp64 codes on nearly every cell."""
+    pkg = _gpu()
+    rng = np.random.default_rng(2000 + seed)
+    cols = _harsh_catalogue(rng, 300)
+    times = np.sort(rng.uniform(-2880.0, 20160.0, 120))
+    s64 = oracle.init_columns(cols, 64)
+    ref64, codes64 = oracle.grid(s64, times, workers=4)
+    g = {k: np.asarray(v, dtype=np.float64)[:, None] for k, v in s64.items()
+         if k != "dtype" and np.asarray(v).ndim}
+    t = times[None, :]
+    simp = np.asarray(s64["isimp"]).astype(bool)[:, None]
+    tempa = 1.0 - g["cc1"] * t - np.where(simp, 0.0, g["d2"] * t**2 + g["d3"] * t**3 + g["d4"] * t**4)
+    em = g["ecco"] - g["bstar"] * g["cc4"] * t
+    regular = (tempa >= 0.2) & (np.abs(em) <= 0.5)
+    res = pkg.propagate_batch(pkg.init_batch(cols, precision=64), times)
+    assert np.array_equal(res.error, codes64)
+    dr, dv = _diff(res.planes, ref64, (codes64 == 0) & regular)
+    assert dr.max(initial=0) <= TOL64_R and dv.max(initial=0) <= TOL64_V
+    r32 = pkg.propagate_batch(pkg.init_batch(cols, precision=32), times)
+    assert (r32.error != codes64).sum() <= 2
+
+
 def test_code_rows_kernel_and_pool_reuse(failure_table, corpus_columns):
     """sgp4b_code_rows flags exactly the rows with a nonzero code (aligned and
     unaligned row strides); propagate_batch zero-fills unflagged rows even
