@@ -212,7 +212,8 @@ def propagate_batch_device(sats: SatBatch, times, out: tuple | None = None,
     process; the grid still lands on the batch's device (see
     :func:`_propagate_device_multi`).  Returns a BatchResult of torch tensors.
     """
-    if devices is not None and len(list(devices)) > 0:
+    devices = list(devices) if devices is not None else []
+    if devices:
         if times_lo is not None:
             raise ValueError("times_lo is not supported with devices=")
         return _propagate_device_multi(sats, times, out, t_absmax, devices)
@@ -455,7 +456,8 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None,
     ``devices`` (e.g. ``range(torch.cuda.device_count())``) spreads the
     satellites over several GPUs of this process (``propagate_batch_multi``).
     """
-    if devices is not None and len(list(devices)) > 0:
+    devices = list(devices) if devices is not None else []
+    if devices:
         return propagate_batch_multi(sats, times, devices)
     t = _times(sats, times)
     dev = sats.device_satrec
