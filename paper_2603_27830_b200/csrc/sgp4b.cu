@@ -665,6 +665,12 @@ __device__ __forceinline__ bool lt_neg(double x, unsigned long long bbits) {
 constexpr long long kBits1em6 = 0x3EB0C6F7A0B5ED8DLL;          // 1.0e-6
 constexpr unsigned long long kBitsM1em3 = 0xBF50624DD2F1A9FCULL; // -0.001
 constexpr unsigned kHi4em3 = 0x3F70624Du;                        // hi word of 0.004
+constexpr unsigned kHiE2 = 0x3FB97F62u;                          // hi word of ~0.0996
+// el2 = axnl^2 + aynl^2 <= (em + |aycof| / pl_lp)^2: below these for every
+// class-1 / class-2 cell of a normal orbit; a collapsed semi-major axis
+// (1/pl_lp large) exceeds them and takes the general cell
+constexpr unsigned kHiEl2K1 = 0x3EFF7510u;                       // hi word of 3e-5
+constexpr unsigned kHiEl2K2 = 0x3F88C7E2u;                       // hi word of 0.0121
 constexpr unsigned kHiTiny = 0x20C00000u;                        // ~6e-151
 
 // Fast fp64 cell for near-circular orbits (|em| < 0.004 at this cell, every
@@ -691,7 +697,13 @@ constexpr unsigned kHiTiny = 0x20C00000u;                        // ~6e-151
 // the caller runs the general cell instead.  The test is per cell, so a
 // cell's value never depends on which other cells share its launch
 // (batch == scalar).
-template <bool ISIMP, class RT, class Trig>
+// K2 = true: the same cell for Kepler class 2 (|em| < 0.0996 at this cell,
+// most of a general LEO catalogue): three Newton steps (error (e/2)^7 e^8
+// < 1e-17), the first rotation by a full table evaluation, exact
+// reciprocals / square roots where class 1 uses series (1/pl_lp, betal,
+// 1/pl, 1/(1 + betal), 1/den).  The J2, drag and orientation stages and the
+// domain fallback are class 1's.
+template <bool ISIMP, class RT, class Trig, bool K2 = false>
 __device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long long re_bits,
                                           double vkm, const Trig& tr, Cell64& o) {
   const int flags = R.flags();
@@ -743,7 +755,7 @@ __device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long
     ok = small_abs(temp, kHi2m6);
   }
   const double asq = __longlong_as_double(dbits(sqam) & 0x7fffffffffffffffLL);   // |sqam|
-  ok = ok && small_abs(em, kHi4em3) &&
+  ok = ok && small_abs(em, K2 ? kHiE2 : kHi4em3) &&
        ((unsigned)__double2hiint(asq) & 0x7fffffffu) >= kHiTiny;
   const bool bad_em = lt_neg(em, kBitsM1em3);
   em = lt_pos(em, kBits1em6) ? 1.0e-6 : em;
@@ -759,35 +771,68 @@ __device__ __forceinline__ bool cell64_c1(const RT& R, double t, double re, long
   tr.short_sin(argpm, sa, ca);
   const double axnl = em * ca;
   const double em2 = em * em;
-  const double ilp = fma(inv_am, fma(em2, em2, em2), inv_am);
+  const double ilp = K2 ? inv_am * rcp64(1.0 - em2)                  // 1 / (am (1 - em^2))
+                        : fma(inv_am, fma(em2, em2, em2), inv_am);
   const double aynl = fma(em, sa, ilp * R[Q_AYCOF]);
   const double u = fma(ilp * R[Q_XLCOF], axnl, usec + nol);
 
-  // Kepler  kernel.py:325-349, two Newton steps from E0 = u
+  // Kepler  kernel.py:325-349, from E0 = u: class 1 two Newton steps,
+  // class 2 three (the reference's freeze at |step| < 1e-12 is reached)
   double s0, c0;
   tr(u, s0, c0);
   double q = fma(c0, axnl, s0 * aynl);
   double num = fma(axnl, s0, -aynl * c0);
-  const double d1 = fma(num, fma(q, q, q), num);
-  const double dd = d1 * d1;
-  const double sd = fma(d1 * dd, K_M1_6, d1);         // d^5/120 < 4e-14
-  const double cd = fma(dd, fma(dd, K_1_24, -0.5), 1.0);
-  const double s1 = fma(s0, cd, c0 * sd), c1 = fma(c0, cd, -s0 * sd);
-  q = fma(c1, axnl, s1 * aynl);
-  num = fma(axnl, s1, fma(-aynl, c1, -d1));
-  const double d2 = fma(num, q, num) * fma(q, q, 1.0);
-  const double sineo1 = fma(c1, d2, s1), coseo1 = fma(-s1, d2, c1);
+  double sineo1, coseo1;
+  if constexpr (K2) {
+    const double d1 = num * rcp64(1.0 - q);             // |d1| <= ~0.11
+    double s1, c1;
+    tr(u + d1, s1, c1);
+    q = fma(c1, axnl, s1 * aynl);
+    num = fma(axnl, s1, fma(-aynl, c1, -d1));
+    const double d2 = num * rcp64(1.0 - q);             // |d2| < 1e-3
+    const double dd = d2 * d2;
+    const double sd = fma(d2 * dd, K_M1_6, d2);          // d^5/120 < 1e-17
+    const double cd = fma(dd, fma(dd, K_1_24, -0.5), 1.0);
+    const double s2 = fma(s1, cd, c1 * sd), c2 = fma(c1, cd, -s1 * sd);
+    q = fma(c2, axnl, s2 * aynl);
+    num = fma(axnl, s2, fma(-aynl, c2, -(d1 + d2)));
+    const double d3 = num * rcp64(1.0 - q);             // |d3| < 1e-8: cos d3 = 1
+    sineo1 = fma(c2, d3, s2);
+    coseo1 = fma(-s2, d3, c2);
+  } else {
+    const double d1 = fma(num, fma(q, q, q), num);
+    const double dd = d1 * d1;
+    const double sd = fma(d1 * dd, K_M1_6, d1);         // d^5/120 < 4e-14
+    const double cd = fma(dd, fma(dd, K_1_24, -0.5), 1.0);
+    const double s1 = fma(s0, cd, c0 * sd), c1 = fma(c0, cd, -s0 * sd);
+    q = fma(c1, axnl, s1 * aynl);
+    num = fma(axnl, s1, fma(-aynl, c1, -d1));
+    const double d2 = fma(num, q, num) * fma(q, q, 1.0);
+    sineo1 = fma(c1, d2, s1);
+    coseo1 = fma(-s1, d2, c1);
+  }
 
   // short-period preliminaries  kernel.py:440-460
   const double ecose = fma(axnl, coseo1, aynl * sineo1);
   const double esine = fma(axnl, sineo1, -aynl * coseo1);
   const double el2 = fma(axnl, axnl, aynl * aynl);
+  ok = ok && small_abs(el2, K2 ? kHiEl2K2 : kHiEl2K1);
   const double ome = 1.0 - ecose;
   const double iome = rcp64(ome);                                 // am / rl
   const double rl = am * ome;
-  const double betal = fma(el2, fma(el2, -0.125, -0.5), 1.0);
-  const double ipl = fma(inv_am, fma(el2, el2, el2), inv_am);
-  const double tq = esine * fma(el2, fma(el2, 0.0625, 0.125), 0.5);
+  double betal, ipl, tq;
+  if constexpr (K2) {
+    // el2 < 0.0121: pl = am (1 - el2) > 0 (no SEMILATUS code)
+    const double omel2 = 1.0 - el2;
+    const double rb = rsqrt64(omel2);
+    betal = omel2 * rb;                                           // sqrt(1 - el2)
+    ipl = inv_am * (rb * rb);                                     // 1 / pl
+    tq = esine * rcp64(1.0 + betal);
+  } else {
+    betal = fma(el2, fma(el2, -0.125, -0.5), 1.0);
+    ipl = fma(inv_am, fma(el2, el2, el2), inv_am);
+    tq = esine * fma(el2, fma(el2, 0.0625, 0.125), 0.5);
+  }
   const double sqvk = (irs * vkm) * iome;                         // sqrt(am)/rl km/s
   const double rdv = sqvk * esine;
   const double rvdv = sqvk * betal;
@@ -1857,6 +1902,9 @@ __device__ __forceinline__ void ld_vec(const double* p, double (&v)[N]) {
 #ifndef SGP4B_ROWPTR
 #define SGP4B_ROWPTR 1
 #endif
+#ifndef SGP4B_F64_K2
+#define SGP4B_F64_K2 1            // fp64 class-2 fast cell (cell64_c1<..., K2 = true>)
+#endif
 #ifndef SGP4B_REC64_REGS
 #define SGP4B_REC64_REGS 0
 #endif
@@ -2125,7 +2173,7 @@ __device__ __forceinline__ void dispatch_row(const RT& R, const float* recg, con
 #endif
 constexpr int kIlp64 = SGP4B_F64_ILP;
 
-template <bool FAST, bool ISIMP, class RT>
+template <bool FAST, bool ISIMP, class RT, bool K2 = false>
 __device__ __forceinline__ void row64(const RT& R, const double* recp, const TrigGrid& tr, double re,
                                       double vkm, int64_t c0, int64_t c1, int lane,
                                       const double* __restrict__ times, int64_t m,
@@ -2150,7 +2198,7 @@ __device__ __forceinline__ void row64(const RT& R, const double* recp, const Tri
 #pragma unroll
     for (int i = 0; i < kIlp64; ++i) {
       if constexpr (FAST) {
-        ok[i] = cell64_c1<ISIMP>(R, t[i], re, dbits(re), vkm, tr, o[i]);
+        ok[i] = cell64_c1<ISIMP, RT, TrigGrid, K2>(R, t[i], re, dbits(re), vkm, tr, o[i]);
       } else {
         cell64_general(R, t[i], re, vkm, tr, o[i]);
         ok[i] = true;
@@ -2185,12 +2233,17 @@ __device__ __forceinline__ void dispatch_row64(const RT& R, const double* recp, 
                                                const double* times, int64_t m, double* row,
                                                int64_t ps, int32_t* crow) {
   const int flags = R.flags();
-  const bool fast = ((flags >> KEPLER_SHIFT) & 0xf) == 1;
-  if (fast) {
+  const int kit = (flags >> KEPLER_SHIFT) & 0xf;
+  if (kit == 1) {
     if (flags & FLAG_ISIMP)
       row64<true, true>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
     else
       row64<true, false>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+  } else if (kit == 2 && SGP4B_F64_K2) {
+    if (flags & FLAG_ISIMP)
+      row64<true, true, RT, true>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
+    else
+      row64<true, false, RT, true>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
   } else {
     row64<false, false>(R, recp, tr, g.re, g.vkm, c0, c1, lane, times, m, row, ps, crow);
   }
