@@ -3,25 +3,33 @@
 // Kernels
 //   init_kernel        1 thread / satellite, fp64.  _sgp4_init, kernel.py:154-322
 //   pack_kernel        1 thread / satellite.  SoA satrec -> packed record
-//   grid_kernel<T>     1 warp = 1 satellite x 128 time steps (4 per lane);
-//                      _propagate + solve_kepler + merge, kernel.py:325-534,
-//                      over the dense grid of propagate_batch, batch.py:166-205
+//   grid_kernel<T>     persistent, 16 warps / SM; a warp walks (satellite,
+//                      128-step chunk) items row by row (4 steps per lane in
+//                      fp32, 1 per lane x 4 in fp64): _propagate +
+//                      solve_kepler + merge, kernel.py:325-534, over the dense
+//                      grid of propagate_batch, batch.py:166-205
 //   (pairs)            sgp4_propagate's broadcasting form (kernel.py:513-534)
 //                      runs through grid_kernel as P one-step rows
 //   kepler_kernel<T>   solve_kepler, kernel.py:325-349
+//   code_rows_kernel   which rows of a code plane hold a nonzero code
+//   tle_columns_kernel TLE catalogue decode (parse_catalog_columns)
+//   drift_norms_kernel, drift_pct_kernel   drift_report, drift.py:46-100
 //
-// Numerics
-//   * fp64 cells follow the reference operation order and its guarded
-//     both-branch selects (dmath.py:199-221); transcendental calls are
-//     CUDA's correctly-rounded-to-1ulp libdevice routines.
+// Numerics (DESIGN.md §4)
+//   * fp64 cells keep the reference's guards, thresholds and code
+//     precedence; they depart from its operation order only far below the
+//     1 mm / 1e-6 km/s budget: per-satellite products folded into the
+//     record, sin/cos from a shared-memory table plus a short polynomial,
+//     small corrections applied as rotations, straight-line fast cells for
+//     Kepler classes 1 and 2 with a per-cell fallback to the general cell.
 //   * fp32 cells are the throughput path: per-satellite work is hoisted into
 //     the packed record at init time (computed in fp64, rounded once), the
-//     secular angles are formed in double-float (hi/lo pairs) and reduced
+//     secular angle is formed in double-float (hi/lo pairs) and reduced
 //     mod 2*pi before anything is rounded to fp32, sin/cos/rcp/rsqrt use the
 //     SFU (MUFU) pipe, Kepler runs a warp-uniform fixed iteration count
-//     chosen from the satellite's eccentricity, atan2 + three of the
+//     chosen from the satellite's eccentricity, atan2 and three of the
 //     sincos evaluations of the short-period stage are replaced by exact
-//     rotations by small angles.
+//     rotations by small angles, and cells run as packed dual-fp32 pairs.
 //   * Error codes follow _first_error precedence 2 > 1 > 4 > 6 and the
 //     init-code merge of kernel.py:497-502, 529-534.
 
