@@ -56,9 +56,12 @@ extern "C" {
  * (kernel.py:316-322).
  *   elements_dev : (7, n) fp64 SoA {no_kozai, ecco, inclo, nodeo, argpo, mo, bstar}
  *   satrec_dev   : (33, n) fp64 SoA out, SatInit float fields in order
+ *                  (may be NULL: the propagate path only needs the records;
+ *                  a later call with the same elements writes the same
+ *                  satrec bit for bit)
  *   init_code_dev: (n) int32 out, error_code_at_init
  *   isimp_dev    : (n) uint8 out
- *   record_dev   : (n, 40) packed T records out (may be NULL) */
+ *   record_dev   : (n, 40) packed T records out (may be NULL; not both) */
 int sgp4b_init(const double* elements_dev, int64_t n, const double* grav,
                int precision, double* satrec_dev, int32_t* init_code_dev,
                uint8_t* isimp_dev, void* record_dev, void* stream);

@@ -61,23 +61,33 @@ def _stream(device) -> int:
 class DeviceSatrec:
     """All per-satellite state of one batch, resident on one GPU.
 
-    satrec : (33, n) fp64, SatInit float fields in dataclass order
+    satrec : (33, n) fp64, SatInit float fields in dataclass order.  The
+             propagate path needs only the records, so batches built from
+             element columns write it on first use (a second init launch over
+             the kept columns, bit-identical) instead of at init time.
     codes  : (n,) int32 error_code_at_init
     isimp  : (n,) uint8
     record : (n, 40) packed propagate records at the batch precision
     """
 
-    satrec: torch.Tensor
+    _satrec: torch.Tensor | None
     codes: torch.Tensor
     isimp: torch.Tensor
     record: torch.Tensor
     precision: int
     grav: GravityModel
     device: torch.device
+    elements: torch.Tensor | None = None      # (7, n) fp64 init input, for the lazy satrec
 
     @property
     def n(self) -> int:
         return int(self.codes.shape[0])
+
+    @property
+    def satrec(self) -> torch.Tensor | None:
+        if self._satrec is None and self.elements is not None:
+            self._satrec = _satrec_of(self.elements, self.grav, self.device)
+        return self._satrec
 
 
 _GRAV_CACHE: dict = {}
@@ -111,19 +121,33 @@ def init_device(elements: np.ndarray, grav: GravityModel, precision: int,
 
 def init_device_tensor(el: torch.Tensor, grav: GravityModel, precision: int,
                        device=None) -> DeviceSatrec:
-    """Same as :func:`init_device` for (7, n) fp64 columns already on the GPU."""
+    """Same as :func:`init_device` for (7, n) fp64 columns already on the GPU
+    (the columns are kept: the public satrec is written on first use)."""
     device = require_cuda(device if device is not None else el.device)
     n = int(el.shape[1])
-    satrec = torch.empty((SATREC_FIELDS, n), dtype=torch.float64, device=device)
     codes = torch.empty((n,), dtype=torch.int32, device=device)
     isimp = torch.empty((n,), dtype=torch.uint8, device=device)
     record = torch.empty((n, RECORD_SLOTS), dtype=torch_dtype(precision), device=device)
     g = _grav_host(grav, device)
     with torch.cuda.device(device):
         _native.check(_native.load().sgp4b_init(
-            el.data_ptr(), n, _host_ptr(g), precision, satrec.data_ptr(),
+            el.data_ptr(), n, _host_ptr(g), precision, None,
             codes.data_ptr(), isimp.data_ptr(), record.data_ptr(), _stream(device)))
-    return DeviceSatrec(satrec, codes, isimp, record, precision, grav, device)
+    return DeviceSatrec(None, codes, isimp, record, precision, grav, device, elements=el)
+
+
+def _satrec_of(el: torch.Tensor, grav: GravityModel, device) -> torch.Tensor:
+    """The (33, n) fp64 satrec of element columns (init kernel, no records)."""
+    n = int(el.shape[1])
+    satrec = torch.empty((SATREC_FIELDS, n), dtype=torch.float64, device=device)
+    codes = torch.empty((n,), dtype=torch.int32, device=device)
+    isimp = torch.empty((n,), dtype=torch.uint8, device=device)
+    g = _grav_host(grav, device)
+    with torch.cuda.device(device):
+        _native.check(_native.load().sgp4b_init(
+            el.data_ptr(), n, _host_ptr(g), 64, satrec.data_ptr(), codes.data_ptr(),
+            isimp.data_ptr(), None, _stream(device)))
+    return satrec
 
 
 def pack_device(satrec64: np.ndarray, codes: np.ndarray, isimp: np.ndarray,

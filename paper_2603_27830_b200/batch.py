@@ -146,7 +146,8 @@ def init_batch(elements: Sequence[MeanElements], grav: GravityModel = WGS72,
         if not elements.is_cuda:
             elements = elements.numpy()
         else:
-            el = elements.to(torch.float64).contiguous()
+            # a private copy: the batch keeps its columns (lazy satrec)
+            el = elements.to(torch.float64).contiguous().clone()
             dev = _device.init_device_tensor(el, grav, _precision(precision), device)
             return SatBatch(device_satrec=dev)
     if isinstance(elements, np.ndarray):
@@ -361,7 +362,7 @@ def _shard_satrec(dev: "_device.DeviceSatrec", lo: int, hi: int, device) -> "_de
     if torch.device(device) != dev.device:
         rec = rec.to(device, non_blocking=True)
         codes = codes.to(device, non_blocking=True)
-    return _device.DeviceSatrec(satrec=None, codes=codes, isimp=None, record=rec,
+    return _device.DeviceSatrec(None, codes=codes, isimp=None, record=rec,
                                 precision=dev.precision, grav=dev.grav,
                                 device=torch.device(device))
 

@@ -1792,8 +1792,10 @@ __global__ void __launch_bounds__(32) init_kernel(
 #pragma unroll
     for (int k = 0; k < 7; ++k) e[k] = el[k * n + i];
     init_one(e, g, f, v, code, simp);
+    if (satrec != nullptr) {
 #pragma unroll
-    for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
+      for (int k = 0; k < F_COUNT; ++k) satrec[k * n + i] = f[k];
+    }
     codes[i] = code;
     isimp[i] = simp ? 1 : 0;
   }
@@ -2785,8 +2787,10 @@ int sgp4b_init(const double* elements_dev, int64_t n, const double* grav, int pr
   if (n <= 0) return fail(SGP4B_EINVAL, "sgp4b_init: n must be positive (got %lld)", (long long)n);
   if (precision != 32 && precision != 64)
     return fail(SGP4B_EINVAL, "sgp4b_init: precision must be 32 or 64, got %d", precision);
-  if (!elements_dev || !satrec_dev || !init_code_dev || !isimp_dev || !grav_from(grav, g))
+  if (!elements_dev || !init_code_dev || !isimp_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_init: null pointer argument");
+  if (!satrec_dev && !record_dev)
+    return fail(SGP4B_EINVAL, "sgp4b_init: neither satrec_dev nor record_dev given");
   // one warp per block: init is a long fp64 dependency chain per thread, so
   // spread the few satellite-warps over as many SMs as possible
   init_kernel<<<blocks_for(n, 32), 32, 0, (cudaStream_t)stream>>>(
