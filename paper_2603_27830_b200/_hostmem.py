@@ -30,7 +30,7 @@ _ALIGN_SMALL = 64 << 10
 _DEFAULT_LIMIT = 4 << 30
 
 _lock = threading.Lock()
-_free: list[tuple[int, int]] = []          # (size, ptr) of retained free blocks
+_free: list[tuple[int, int, int]] = []     # (size, ptr, release order) of retained free blocks
 # blocks released by PinnedBlock.__del__: a finalizer may run inside any
 # allocation (GC), even while this module holds _lock, so it never takes the
 # lock; it appends here (deque.append is atomic) and the next pool call
@@ -74,19 +74,33 @@ class PinnedBlock:
             self.ptr = 0
 
 
+_age = [0]                                   # release order of the free blocks
+
+
 def _drain() -> list[int]:
     """Move released blocks into the free list (caller holds _lock); returns
-    the pointers beyond the cache limit, to be unpinned outside the lock."""
+    the pointers to unpin outside the lock.  The most recently released
+    blocks are kept: a block that does not fit under the cache limit evicts
+    the least recently released free blocks first (a large grid that is
+    re-requested call after call stays pinned even after smaller tiles
+    filled the cache); only a block larger than the limit itself is freed."""
     excess = []
     limit = cache_limit()
     while _released:
         size, ptr = _released.popleft()
-        if _stats["cached_bytes"] + size <= limit:
-            _free.append((size, ptr))
-            _stats["cached_bytes"] += size
-        else:
+        if size > limit:
             _stats["pinned_bytes"] -= size
             excess.append(ptr)
+            continue
+        while _free and _stats["cached_bytes"] + size > limit:
+            k = min(range(len(_free)), key=lambda i: _free[i][2])     # oldest
+            osize, optr, _ = _free.pop(k)
+            _stats["cached_bytes"] -= osize
+            _stats["pinned_bytes"] -= osize
+            excess.append(optr)
+        _age[0] += 1
+        _free.append((size, ptr, _age[0]))
+        _stats["cached_bytes"] += size
     _free.sort()
     return excess
 
@@ -105,7 +119,7 @@ def alloc(nbytes: int) -> PinnedBlock:
     hit = None
     with _lock:
         excess = _drain()
-        for k, (sz, ptr) in enumerate(_free):
+        for k, (sz, ptr, _) in enumerate(_free):
             if sz >= size and sz <= size + size // 2:
                 del _free[k]
                 _stats["cached_bytes"] -= sz
@@ -192,8 +206,8 @@ def empty_cache() -> None:
         blocks = list(_free)
         _free.clear()
         _stats["cached_bytes"] = 0
-        _stats["pinned_bytes"] -= sum(s for s, _ in blocks)
-    for ptr in excess + [p for _, p in blocks]:
+        _stats["pinned_bytes"] -= sum(b[0] for b in blocks)
+    for ptr in excess + [b[1] for b in blocks]:
         _free_ptr(ptr)
 
 

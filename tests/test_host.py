@@ -284,3 +284,59 @@ def test_ingest_host_lines_follow_read_tle_file(tmp_path):
     with pytest.raises(TleError, match="line 2 missing"):
         _host_lines(_as_bytes(f"{a}\n{a}\n{b}\n".encode()))
     assert _as_bytes(b"xy").flags.writeable
+
+
+def test_pinned_pool_keeps_recent_blocks(monkeypatch):
+    """The pinned pool (with a fake allocator, no GPU) caches the most
+    recently released blocks under its limit, evicting the oldest first, so
+    a large grid requested call after call stays cached after smaller tiles
+    filled the pool; a block larger than the limit is never cached."""
+    import ctypes
+    import gc
+    from paper_2603_27830_b200 import _hostmem
+    libc = ctypes.CDLL(None)
+    libc.malloc.restype = ctypes.c_void_p
+    libc.malloc.argtypes = [ctypes.c_size_t]
+    libc.free.argtypes = [ctypes.c_void_p]
+    live = {}
+
+    class FakeLib:
+        def sgp4b_host_alloc(self, size, out):
+            p = libc.malloc(size)
+            live[p] = size
+            ctypes.cast(out, ctypes.POINTER(ctypes.c_void_p))[0] = p
+            return 0
+
+        def sgp4b_host_free(self, p):
+            libc.free(live.pop(p) and p)
+            return 0
+
+        def sgp4b_last_error(self):
+            return b""
+
+    monkeypatch.setattr(_hostmem._native, "load", lambda: FakeLib())
+    _hostmem._free.clear()
+    _hostmem._released.clear()
+    monkeypatch.setitem(_hostmem._stats, "cached_bytes", 0)
+    monkeypatch.setitem(_hostmem._stats, "pinned_bytes", 0)
+    mb = 1 << 20
+    monkeypatch.setenv("SGP4B_HOST_CACHE_BYTES", str(20 * mb))
+    tiles = [_hostmem.alloc(4 * mb) for _ in range(4)]          # 16 MiB of tiles
+    del tiles
+    gc.collect()
+    assert _hostmem.stats()["cached_bytes"] == 16 * mb
+    big = _hostmem.alloc(12 * mb)
+    del big
+    gc.collect()
+    st = _hostmem.stats()                                      # oldest tiles evicted
+    assert st["cached_bytes"] <= 20 * mb and any(b[0] == 12 * mb for b in _hostmem._free)
+    reuses = st["reuses"]
+    again = _hostmem.alloc(12 * mb)
+    assert _hostmem.stats()["reuses"] == reuses + 1
+    del again
+    huge = _hostmem.alloc(30 * mb)                              # above the limit
+    del huge
+    gc.collect()
+    assert all(b[0] != 30 * mb for b in _hostmem._free)
+    _hostmem.empty_cache()
+    assert not live
