@@ -46,6 +46,34 @@ def cache_limit() -> int:
     return int(v) if v else _DEFAULT_LIMIT
 
 
+_PIN_EAGER = 256 << 20
+_recent: collections.OrderedDict = collections.OrderedDict()   # recently requested sizes
+
+
+def worth_pinning(nbytes: int) -> bool:
+    """Whether a result of ``nbytes`` should land in a pinned block (fast
+    D2H, pooled) rather than in pageable memory filled through the staging
+    ring.  Page-locking costs ~0.4 s/GB, so a large block is pinned only
+    when it will pay back: one of that size is already cached, or the same
+    size was requested recently (a repeated call: the second pins, later
+    ones reuse it).  Small results (<= 256 MiB) are always pinned.  Every
+    call is remembered."""
+    size = _round(max(int(nbytes), 1))
+    if size > cache_limit():
+        return False
+    with _lock:
+        excess = _drain()
+        seen = size in _recent
+        _recent[size] = None
+        _recent.move_to_end(size)
+        while len(_recent) > 16:
+            _recent.popitem(last=False)
+        cached = any(sz >= size and sz <= size + size // 2 for sz, _, _ in _free)
+    for ptr in excess:
+        _free_ptr(ptr)
+    return size <= _PIN_EAGER or cached or seen
+
+
 def _round(nbytes: int) -> int:
     a = _ALIGN_LARGE if nbytes >= _ALIGN_LARGE else _ALIGN_SMALL
     return -(-nbytes // a) * a

@@ -393,7 +393,7 @@ def propagate_batch_multi(sats: SatBatch, times, devices) -> BatchResult:
     n, m = sats.n, t.size
     devs = _devices(devices)
     itemsize = 4 if dev.precision == 32 else 8
-    staged = n * m * (6 * itemsize + 4) > _hostmem.cache_limit()
+    staged = not _hostmem.worth_pinning(n * m * (6 * itemsize + 4) + n)
     planes_h, error_h, flags_h = (_host_grid_pageable if staged else _host_grid)(n, m,
                                                                                  dev.precision)
     t_abs = _device.times_absmax(t)
@@ -464,7 +464,7 @@ def propagate_batch(sats: SatBatch, times, workers: int | None = None,
     dev = sats.device_satrec
     n, m = sats.n, t.size
     itemsize = 4 if dev.precision == 32 else 8
-    staged = n * m * (6 * itemsize + 4) > _hostmem.cache_limit()
+    staged = not _hostmem.worth_pinning(n * m * (6 * itemsize + 4) + n)
     planes_h, error_h, flags_h = (_host_grid_pageable if staged else _host_grid)(n, m,
                                                                                  dev.precision)
     with torch.cuda.device(dev.device):
