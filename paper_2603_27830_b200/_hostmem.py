@@ -213,18 +213,25 @@ def _pool():
     return _fill_pool
 
 
+_ZERO_PARTS = 4
+
+
 def zero_fill_async(arr: np.ndarray, lo: int, hi: int) -> list:
-    """Zero rows lo..hi of a C-contiguous array in ``_ZERO_CHUNK`` pieces on
-    a small thread pool (``ctypes.memset`` releases the GIL, so the fill runs
-    while the caller waits on a DMA).  Returns the futures."""
+    """Zero rows lo..hi of a C-contiguous array on the host thread pool
+    (``ctypes.memset`` releases the GIL, so the fill runs while the caller
+    waits on a DMA), in at most ``_ZERO_PARTS`` pieces of at least
+    ``_ZERO_CHUNK`` bytes: more concurrent fills only compete with the DMA
+    for host memory bandwidth (C4: 4 threads 64 ms, 16 threads 67 ms, against
+    a 60.4 ms planes copy).  Returns the futures."""
     if hi <= lo:
         return []
     row = arr.strides[0]
     base = arr.ctypes.data + lo * row
     total = (hi - lo) * row
+    piece = max(_ZERO_CHUNK, -(-total // _ZERO_PARTS))
     pool = _pool()
-    return [pool.submit(ctypes.memset, base + off, 0, min(_ZERO_CHUNK, total - off))
-            for off in range(0, total, _ZERO_CHUNK)]
+    return [pool.submit(ctypes.memset, base + off, 0, min(piece, total - off))
+            for off in range(0, total, piece)]
 
 
 def empty_cache() -> None:
