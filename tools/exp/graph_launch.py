@@ -22,7 +22,7 @@ rd = torch.ones(64 << 20, device=dev)
 sink = torch.empty((), device=dev)
 
 def launch():
-    _device.propagate_grid(sats.device_satrec, t, planes, codes)
+    _device.propagate_grid(sats.device_satrec, t, planes, codes, t_absmax=1440.0)
 
 s = torch.cuda.Stream()
 s.wait_stream(torch.cuda.current_stream())

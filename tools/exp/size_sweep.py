@@ -29,7 +29,7 @@ for n in (296, 1184, 2368, 4736, 9341, 18682, 37364, 74728):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        _device.propagate_grid(sats.device_satrec, times, planes, codes)
+        _device.propagate_grid(sats.device_satrec, times, planes, codes, t_absmax=1440.0)
         b.record()
         torch.cuda.synchronize()
         if k >= 5:

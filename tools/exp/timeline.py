@@ -29,7 +29,7 @@ for k in range(4):
     flush.fill_(k)
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record()
-    _device.propagate_grid(sats.device_satrec, times, planes, codes)
+    _device.propagate_grid(sats.device_satrec, times, planes, codes, t_absmax=1440.0)
     b.record()
     torch.cuda.synchronize()
 warps = 148 * 16
