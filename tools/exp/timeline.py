@@ -43,3 +43,4 @@ q = lambda x: [round(float(v), 2) for v in np.percentile(x, [0, 10, 50, 90, 100]
 print(json.dumps({"event_us": a.elapsed_time(b) * 1e3, "start_us_pct": q(st),
                   "first_row_done_us_pct": q(fr), "end_us_pct": q(en),
                   "sms": int(np.unique(buf[:, 3]).size)}, indent=1))
+np.save(str(ROOT / "gpurun_out" / f"timeline_{n}.npy"), buf)
