@@ -2265,14 +2265,13 @@ __device__ __forceinline__ void dispatch_row64(const RT& R, const double* recp, 
 
 
 //
-// The same kernel instance (VEC = true) also serves the scalar/broadcasting
+// The fp64 instance (VEC = true) also serves the fp64 scalar/broadcasting
 // API: with rec_idx set, row r uses record rec_idx[r] and times + r*times_ld,
-// so a list of (satellite, time) pairs runs as P rows of one step (never the
-// vector path) through exactly the instructions that compute an aligned
-// dense grid: batch == scalar bit for bit, whatever contraction choices the
-// compiler made.  The Python layer pads unaligned grids so every public call
-// runs this instance; VEC = false only serves raw C-ABI callers with
-// unaligned strides.
+// so a list of (satellite, time) pairs runs as P rows of one step through
+// exactly the instructions that compute a dense grid (fp32 pairs have their
+// own one-lane-per-pair kernel, pairs_kernel32).  The Python layer pads
+// unaligned grids so every public call runs the VEC instance; VEC = false
+// only serves raw C-ABI callers with unaligned strides.
 #ifdef SGP4B_TIMELINE
 // analysis build: per-warp (start, first row done, end, smid) in ns
 constexpr int kTimelineWarps = 1 << 16;
@@ -2383,6 +2382,71 @@ grid_kernel(const T* __restrict__ rec, const int64_t* __restrict__ rec_idx, int6
     g_timeline[w][3] = smid;
   }
 #endif
+}
+
+// Elementwise pairs (scalar / broadcasting API), fp32: one lane per
+// (satellite, time) pair.  A pair runs the same cellv instance a grid row of
+// its satellite runs (chosen by the same (isimp, Kepler class) rule and the
+// same t_crit / t_absmax test as dispatch_row + fixup_row), with both halves
+// of the packed pair set to its time.  Every mul/add/fma of cellv is an
+// explicit IEEE-rounded op and every SFU/select is per component, so the
+// pair's value equals the grid cell's bit for bit however the record is held
+// (per-lane registers here, warp-uniform registers in the grid).  Lanes of a
+// warp may take different classes; each class runs once per warp.
+#ifndef SGP4B_PAIRS_LANE
+#define SGP4B_PAIRS_LANE 1
+#endif
+constexpr int kPairsBlock = 128;
+
+template <bool LO>
+__global__ void __launch_bounds__(kPairsBlock) pairs_kernel32(
+    const float* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t p,
+    const float* __restrict__ times, const float* __restrict__ times_lo, Grav g,
+    float* __restrict__ rv, int32_t* __restrict__ codes, float t_absmax) {
+  const int64_t k = (int64_t)blockIdx.x * kPairsBlock + threadIdx.x;
+  if (k >= p) return;
+  const int64_t ri = __ldg(rec_idx + k);
+  Rec<float> R;
+  load_rec(rec + ri * S_COUNT, R);
+  const float t = __ldg(times + k);
+  const float tl = LO ? __ldg(times_lo + k) : 0.0f;
+  const int flags = R.flags();
+  int kit = (flags >> KEPLER_SHIFT) & 0xf;
+  const bool simp = flags & FLAG_ISIMP;
+  if (kit >= 1 && kit <= 3) {
+    // dispatch_row's t_crit and its masked general pass (fixup_row)
+    const float bound = kit == 1 ? 0.004f : kit == 2 ? 0.1f : 0.4f;
+    const float slack = bound - fabsf(R[P_E0]) - 2.0f * fabsf(R[P_BC5]);
+    const float t_crit = slack > 0.0f ? slack / fabsf(R[P_BC4]) : -1.0f;
+    if (!(t_absmax <= t_crit) && fabsf(t) > t_crit) kit = 0;
+  }
+  // the second half is the same time through an opaque move, so the
+  // compiler cannot see that the halves are equal and fold the packed pair
+  // into scalar ops (whose contraction it could then choose differently):
+  // the pair runs the packed instruction stream of a grid cell
+  float t2, tl2;
+  asm("mov.b32 %0, %1;" : "=f"(t2) : "f"(t));
+  asm("mov.b32 %0, %1;" : "=f"(tl2) : "f"(tl));
+  VN<2> tv, tlv, o[6];
+  tv.h[0] = make_float2(t, t2);
+  tlv.h[0] = make_float2(tl, tl2);
+  int cv[2];
+#define SGP4B_PAIR(S, K) cellv<S, K, LO, 2>(R, tv, tlv, g, o, cv)
+  if (!simp) {
+    if (kit == 1) SGP4B_PAIR(false, 1);
+    else if (kit == 2) SGP4B_PAIR(false, 2);
+    else if (kit == 3) SGP4B_PAIR(false, 3);
+    else SGP4B_PAIR(false, 0);
+  } else {
+    if (kit == 1) SGP4B_PAIR(true, 1);
+    else if (kit == 2) SGP4B_PAIR(true, 2);
+    else if (kit == 3) SGP4B_PAIR(true, 3);
+    else SGP4B_PAIR(true, 0);
+  }
+#undef SGP4B_PAIR
+#pragma unroll
+  for (int q = 0; q < 6; ++q) st_cs(rv + q * p + k, o[q].h[0].x);
+  st_cs(codes + k, cv[0]);
 }
 
 template <typename T>
@@ -2847,6 +2911,25 @@ int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, co
     return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: precision must be 32 or 64, got %d", precision);
   if (!record_dev || !sat_idx_dev || !times_dev || !rv_dev || !codes_dev || !grav_from(grav, g))
     return fail(SGP4B_EINVAL, "sgp4b_propagate_pairs: null pointer argument");
+#if SGP4B_PAIRS_LANE
+  if (precision == 32) {
+    const float* tlo = static_cast<const float*>(times_lo_dev);
+    // launch_grid's bound: |t| rounded up into fp32, NaN stays NaN
+    float tb = (float)t_absmax;
+    if ((double)tb < t_absmax) tb = nextafterf(tb, INFINITY);
+    const unsigned blocks = (unsigned)((p + kPairsBlock - 1) / kPairsBlock);
+    if (tlo != nullptr)
+      pairs_kernel32<true><<<blocks, kPairsBlock, 0, (cudaStream_t)stream>>>(
+          static_cast<const float*>(record_dev), sat_idx_dev, p,
+          static_cast<const float*>(times_dev), tlo, g, static_cast<float*>(rv_dev), codes_dev, tb);
+    else
+      pairs_kernel32<false><<<blocks, kPairsBlock, 0, (cudaStream_t)stream>>>(
+          static_cast<const float*>(record_dev), sat_idx_dev, p,
+          static_cast<const float*>(times_dev), nullptr, g, static_cast<float*>(rv_dev), codes_dev,
+          tb);
+    return check_launch("sgp4b_propagate_pairs");
+  }
+#endif
   // P rows of one step: row k = record sat_idx[k] at times[k]; output (6, P).
   // The VEC instance (m = 1 never takes its vector path) is the one aligned
   // grids use, so a pair equals the corresponding grid cell bit for bit.

@@ -1081,3 +1081,115 @@ def test_multi_device_path_bitwise(corpus_columns, failure_table, precision, nde
     multi = pkg.propagate_batch(sats, times, devices=devs)
     assert np.array_equal(multi.planes, single.planes, equal_nan=True)
     assert np.array_equal(multi.error, single.error)
+
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_pairs_equal_grid_cells_every_class(corpus_columns, precision, seed):
+    """The elementwise pairs path (fp32: one lane per pair, its own kernel)
+    equals the grid cell of the same (satellite, t) bit for bit, on every
+    (isimp, Kepler class), on cells that leave their class's domain (heavy
+    drag, +-14 days), on failing cells, and whatever t_absmax bound the
+    caller passes; the pair order is shuffled so a warp mixes classes."""
+    import torch
+    from paper_2603_27830_b200 import _device
+    pkg = _gpu()
+    rng = np.random.default_rng(4100 + seed)
+    heavy = corpus_columns[:, [137, 415, 391]].copy()
+    heavy[1] = [0.0029, 0.05, 0.2]
+    heavy[6] = [1e-2, -1e-2, 1e-2]
+    cols = np.concatenate([_harsh_catalogue(rng, 2000), corpus_columns[:, ::7], heavy], axis=1)
+    n = cols.shape[1]
+    times = np.sort(np.concatenate([rng.uniform(-20160.0, 20160.0, 150), [0.0, 1440.0]]))
+    m = times.size
+    npdt = np.float32 if precision == 32 else np.float64
+    sats = pkg.init_batch(cols, precision=precision)
+    grid = pkg.propagate_batch_device(sats, times)
+    dev = grid.planes.device
+    order = rng.permutation(n * m)
+    ii, jj = np.divmod(order, m)
+    idx = torch.from_numpy(ii.astype(np.int64)).to(dev)
+    jdx = torch.from_numpy(jj.astype(np.int64)).to(dev)
+    t_pairs = torch.from_numpy(times[jj].astype(npdt)).to(dev)
+    want_p = grid.planes[:, idx, jdx]
+    want_c = grid.error[idx, jdx]
+    assert int((want_c != 0).sum()) > 0
+    if precision == 32:
+        # every (isimp, Kepler class) instance of the cell is exercised
+        flags = sats.device_satrec.record[:, 33].contiguous().view(torch.int32).cpu().numpy()
+        kit = (flags >> 4) & 0xF
+        kit = np.where((kit >= 1) & (kit <= 3), kit, 0)     # 0: the general cell
+        combos = set(zip((flags & 1).tolist(), kit.tolist()))
+        assert combos >= {(s_, k_) for s_ in (0, 1) for k_ in (0, 1, 2, 3)}, combos
+    for bound in (None, float("inf"), float("nan")):
+        rv = torch.empty((6, n * m), dtype=want_p.dtype, device=dev)
+        codes = torch.empty((n * m,), dtype=torch.int32, device=dev)
+        _device.propagate_pairs(sats.device_satrec, idx, t_pairs, rv, codes, t_absmax=bound)
+        same = (rv == want_p) | (torch.isnan(rv) & torch.isnan(want_p))
+        assert bool(same.all()), f"{int((~same.all(0)).sum())} pairs differ (bound {bound})"
+        assert torch.equal(codes, want_c)
+    # the public general broadcast: satellite i at its own time
+    js = rng.integers(0, m, n)
+    sd = pkg.sgp4_propagate(sats.init, times[js].astype(npdt))
+    host = grid.planes[:, torch.arange(n, device=dev), torch.from_numpy(js).to(dev)].cpu().numpy()
+    assert np.array_equal(sd.r.T, host[:3], equal_nan=True)
+    assert np.array_equal(sd.v.T, host[3:], equal_nan=True)
+    assert np.array_equal(sd.error_code, grid.error[torch.arange(n, device=dev),
+                                                    torch.from_numpy(js).to(dev)].cpu().numpy())
+
+
+def test_pairs_times_lo_equal_grid_cells(corpus_columns):
+    """C-ABI pairs with fp32 low words (t = hi + lo) equal the grid cells of
+    the times_lo grid launch bit for bit."""
+    import torch
+    from paper_2603_27830_b200 import _device, _native
+    pkg = _gpu()
+    rng = np.random.default_rng(77)
+    cols = np.concatenate([_harsh_catalogue(rng, 200), corpus_columns[:, ::11]], axis=1)
+    n = cols.shape[1]
+    times = np.sort(rng.uniform(-10080.0, 20160.0, 97))
+    hi = times.astype(np.float32)
+    lo = (times - hi.astype(np.float64)).astype(np.float32)
+    sats = pkg.init_batch(cols, precision=32)
+    dev = torch.device("cuda", 0)
+    t_hi, t_lo = torch.from_numpy(hi).to(dev), torch.from_numpy(lo).to(dev)
+    grid = pkg.propagate_batch_device(sats, t_hi, times_lo=t_lo)
+    ii, jj = np.divmod(rng.permutation(n * times.size), times.size)
+    idx = torch.from_numpy(ii.astype(np.int64)).to(dev)
+    jdx = torch.from_numpy(jj.astype(np.int64)).to(dev)
+    p = int(idx.numel())
+    rv = torch.empty((6, p), dtype=torch.float32, device=dev)
+    codes = torch.empty((p,), dtype=torch.int32, device=dev)
+    tp_hi, tp_lo = t_hi[jdx].contiguous(), t_lo[jdx].contiguous()
+    d = sats.device_satrec
+    _native.check(_native.load().sgp4b_propagate_pairs(
+        d.record.data_ptr(), idx.data_ptr(), tp_hi.data_ptr(), tp_lo.data_ptr(), p,
+        float(np.abs(times).max()), 32, _device._host_ptr(_device._grav_host(d.grav, dev)),
+        rv.data_ptr(), codes.data_ptr(), _device._stream(dev)))
+    want = grid.planes[:, idx, jdx]
+    assert bool(((rv == want) | (torch.isnan(rv) & torch.isnan(want))).all())
+    assert torch.equal(codes, grid.error[idx, jdx])
+
+
+def test_pairs_equal_grid_c2_every_cell():
+    """All 9,341,000 cells of the C2 workload (Starlink-like catalogue x
+    linspace(0, 1440, 1000), fp32) as shuffled elementwise pairs: equal to
+    the dense grid bit for bit."""
+    import torch
+    from paper_2603_27830_b200 import _device
+    from paper_2603_27830_b200.catalog import starlink_like
+    pkg = _gpu()
+    n, m = 9341, 1000
+    times = np.linspace(0.0, 1440.0, m)
+    sats = pkg.init_batch(starlink_like(n), precision=32)
+    grid = pkg.propagate_batch_device(sats, times)
+    dev = grid.planes.device
+    perm = torch.randperm(n * m, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    idx, jdx = perm // m, perm % m
+    t_pairs = torch.from_numpy(times.astype(np.float32)).to(dev)[jdx].contiguous()
+    rv = torch.empty((6, n * m), dtype=torch.float32, device=dev)
+    codes = torch.empty((n * m,), dtype=torch.int32, device=dev)
+    _device.propagate_pairs(sats.device_satrec, idx.contiguous(), t_pairs, rv, codes)
+    assert torch.equal(rv, grid.planes[:, idx, jdx])
+    assert torch.equal(codes, grid.error[idx, jdx])
