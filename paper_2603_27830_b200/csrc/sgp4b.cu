@@ -2265,13 +2265,12 @@ __device__ __forceinline__ void dispatch_row64(const RT& R, const double* recp, 
 
 
 //
-// The fp64 instance (VEC = true) also serves the fp64 scalar/broadcasting
-// API: with rec_idx set, row r uses record rec_idx[r] and times + r*times_ld,
-// so a list of (satellite, time) pairs runs as P rows of one step through
-// exactly the instructions that compute a dense grid (fp32 pairs have their
-// own one-lane-per-pair kernel, pairs_kernel32).  The Python layer pads
-// unaligned grids so every public call runs the VEC instance; VEC = false
-// only serves raw C-ABI callers with unaligned strides.
+// With rec_idx set, row r uses record rec_idx[r] and times + r*times_ld:
+// (satellite, time) pairs as P rows of one step.  The elementwise API uses
+// this only when built with SGP4B_PAIRS_LANE=0 (pairs_kernel32/64 run one
+// lane per pair).  The Python layer pads unaligned grids so every public
+// call runs the VEC instance; VEC = false only serves raw C-ABI callers with
+// unaligned strides.
 #ifdef SGP4B_TIMELINE
 // analysis build: per-warp (start, first row done, end, smid) in ns
 constexpr int kTimelineWarps = 1 << 16;
@@ -2447,6 +2446,62 @@ __global__ void __launch_bounds__(kPairsBlock) pairs_kernel32(
 #pragma unroll
   for (int q = 0; q < 6; ++q) st_cs(rv + q * p + k, o[q].h[0].x);
   st_cs(codes + k, cv[0]);
+}
+
+// Elementwise pairs, fp64: one lane per pair, grid-stride over the pairs so
+// each block builds the shared (sin, cos) table once.  A lane reads its
+// record through RecS<double> pointed at global memory (the grid kernel's
+// record type, pointed at shared memory there) and runs the cell the grid's
+// dispatch_row64 picks for that record: cell64_c1 (class 1, or class 2 with
+// K2) with the out-of-line general cell as its per-cell fallback, else the
+// general cell.
+constexpr int kPairsBlock64 = 256;
+
+__global__ void __launch_bounds__(kPairsBlock64) pairs_kernel64(
+    const double* __restrict__ rec, const int64_t* __restrict__ rec_idx, int64_t p,
+    const double* __restrict__ times, Grav g, double* __restrict__ rv,
+    int32_t* __restrict__ codes) {
+  __shared__ double2 sintab[kTabN];
+  for (int i = threadIdx.x; i < kTabN; i += kPairsBlock64) {
+    double sv, cv;
+    sincospi((double)i / (kTabN / 2), &sv, &cv);
+    sintab[i] = make_double2(sv, cv);
+  }
+  __syncthreads();
+  const TrigGrid tr{sintab};
+  const double re = g.re, vkm = g.vkm;
+  for (int64_t k = (int64_t)blockIdx.x * kPairsBlock64 + threadIdx.x; k < p;
+       k += (int64_t)gridDim.x * kPairsBlock64) {
+    const double* recp = rec + __ldg(rec_idx + k) * S_COUNT;
+    RecS<double> R;
+    R.p = recp;
+    const double t = __ldg(times + k);
+    const int flags = R.flags();
+    const int kit = (flags >> KEPLER_SHIFT) & 0xf;
+    const bool simp = flags & FLAG_ISIMP;
+    Cell64 o;
+    bool ok = true;
+    if (kit == 1) {
+      ok = simp ? cell64_c1<true, RecS<double>, TrigGrid, false>(R, t, re, dbits(re), vkm, tr, o)
+                : cell64_c1<false, RecS<double>, TrigGrid, false>(R, t, re, dbits(re), vkm, tr, o);
+    } else if (kit == 2 && SGP4B_F64_K2) {
+      ok = simp ? cell64_c1<true, RecS<double>, TrigGrid, true>(R, t, re, dbits(re), vkm, tr, o)
+                : cell64_c1<false, RecS<double>, TrigGrid, true>(R, t, re, dbits(re), vkm, tr, o);
+    } else {
+      cell64_general(R, t, re, vkm, tr, o);
+    }
+    if (!ok) {
+      cell64_fallback(recp, t, re, vkm, sintab, rv + k, p, codes + k);
+      continue;
+    }
+    st_cs(rv + k, o.r[0]);
+    st_cs(rv + p + k, o.r[1]);
+    st_cs(rv + 2 * p + k, o.r[2]);
+    st_cs(rv + 3 * p + k, o.v[0]);
+    st_cs(rv + 4 * p + k, o.v[1]);
+    st_cs(rv + 5 * p + k, o.v[2]);
+    st_cs(codes + k, o.code);
+  }
 }
 
 template <typename T>
@@ -2927,6 +2982,18 @@ int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev, co
           static_cast<const float*>(record_dev), sat_idx_dev, p,
           static_cast<const float*>(times_dev), nullptr, g, static_cast<float*>(rv_dev), codes_dev,
           tb);
+    return check_launch("sgp4b_propagate_pairs");
+  }
+  if (precision == 64) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      return fail(SGP4B_ECUDA, "sgp4b_propagate_pairs: device query failed");
+    const int64_t need = (p + kPairsBlock64 - 1) / kPairsBlock64;
+    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)sms * 4);   // 4 resident per SM
+    pairs_kernel64<<<blocks, kPairsBlock64, 0, (cudaStream_t)stream>>>(
+        static_cast<const double*>(record_dev), sat_idx_dev, p,
+        static_cast<const double*>(times_dev), g, static_cast<double*>(rv_dev), codes_dev);
     return check_launch("sgp4b_propagate_pairs");
   }
 #endif
