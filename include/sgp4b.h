@@ -102,7 +102,8 @@ int sgp4b_propagate_grid(const void* record_dev, int64_t n,
 /* Elementwise pairs: cell k = satellite sat_idx[k] at times[k].  Replaces
  * the broadcasting scalar sgp4_propagate (kernel.py:513-534).  Each pair
  * equals the sgp4b_propagate_grid cell of the same (record, time, time low
- * word, t_absmax) bit for bit.
+ * word, t_absmax) bit for bit.  Every sat_idx[k] must index a record of
+ * record_dev (the call has no record count to check it against).
  *   rv_dev : (6, p) T out; codes_dev : (p) int32 out. */
 int sgp4b_propagate_pairs(const void* record_dev, const int64_t* sat_idx_dev,
                           const void* times_dev, const float* times_lo_dev,
